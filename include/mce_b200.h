@@ -1,0 +1,125 @@
+/*
+ * mce_b200.h -- C ABI of the B200 maximal-clique-enumeration engine
+ * (libmce_b200.so, built from paper_2212_01473_b200/csrc/).
+ *
+ * This is the drop-in boundary for the hot path of the reference `mce`
+ * package (a Python implementation of arXiv:2212.01473 at
+ * /root/reference/pkg/src/mce).  Each entry point replaces one reference
+ * function; the Python host layer (paper_2212_01473_b200/, ctypes) mirrors
+ * the reference API on top of these calls.  Plain pointers and sizes only.
+ *
+ *   reference function                          replaced by
+ *   graph.py:96-120   from_edges            ->  mce_graph_from_edges
+ *   graph.py:123-175  parse_edge_list (tail)->  mce_graph_from_edges (after host tokenising)
+ *   graph.py:29-50    Graph CSR accessors   ->  mce_graph_from_csr / mce_graph_copy_csr / mce_graph_info
+ *   graph.py:189-218  degeneracy_order      ->  mce_degeneracy_order
+ *   graph.py:221-232  reorder               ->  mce_reorder
+ *   graph.py:235-243  stats / preprocess    ->  mce_graph_info (+ the two above)
+ *   scheduler.py:441-492 run (+ bk.py roots, induced.py, xsets.py, the worker list)
+ *                                           ->  mce_enumerate
+ *
+ * Error behaviour: every call returns 0 on success and a negative code on
+ * failure, with a message from mce_last_error():
+ *   -1  CUDA error (allocation, launch, ...)
+ *   -2  invalid argument (reference: ValueError)
+ *   -3  device limits (a kernel variant does not fit)
+ *   -4  capacity exceeded (reference: induced.CapacityError)
+ *
+ * Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  All
+ * calls are synchronous with respect to the host on return.
+ */
+#ifndef MCE_B200_H
+#define MCE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCE_HIST_MAX 4096
+
+typedef struct mce_graph mce_graph; /* device-resident canonical CSR */
+
+const char* mce_last_error(void);
+
+/* Canonical graph from (u, v) pairs: self-loops dropped, duplicates merged,
+ * symmetric, rows strictly ascending (graph.py:96-120).  `edges` holds
+ * 2*num_edges int64 values, on the host or (edges_on_device=1) the device. */
+int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
+                         int edges_on_device, void* stream, mce_graph** out);
+
+/* Adopt an already canonical CSR (row_offsets: n+1, col_indices: nnz). */
+int mce_graph_from_csr(const int64_t* row_offsets, const int64_t* col_indices, int64_t n,
+                       int64_t nnz, int on_device, void* stream, mce_graph** out);
+
+/* n, directed entries (2m), max degree, max later / earlier neighbour counts. */
+int mce_graph_info(const mce_graph* g, int64_t* n, int64_t* nnz, int64_t* max_degree,
+                   int64_t* max_later, int64_t* max_earlier);
+
+/* Copy the CSR (and, when present, the original labels) to host buffers. */
+int mce_graph_copy_csr(const mce_graph* g, int64_t* row_offsets, int64_t* col_indices,
+                       int64_t* labels, void* stream);
+
+void mce_graph_free(mce_graph* g);
+
+/* Degeneracy ordering (graph.py:189-218): position[v] = rank of v.
+ *   method 1: the reference's exact order (minimum current degree, ties to the
+ *             smallest id) -- bit-identical positions, single-CTA kernel;
+ *   method 0: parallel bucket peeling -- a valid degeneracy order with the same
+ *             degeneracy, vertices of one peel round ranked by id. */
+int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
+                         int position_on_device, int64_t* degeneracy, void* stream);
+
+/* Relabel by position (graph.py:221-232).  The result remembers the original
+ * label of every vertex (used to hash cliques by original ids). */
+int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_device,
+                void* stream, mce_graph** out);
+
+typedef struct {
+  int roots;             /* 1 = first-level (per vertex), 2 = second-level (per edge) */
+  int induced_full;      /* 1 = full ("ipx"), 0 = partial ("ip") */
+  int workers;           /* worker warps; 0 = every co-resident warp */
+  int worker_list;       /* donation protocol on/off (RunConfig.worker_list) */
+  int donation_min_p;    /* RunConfig.donation_min_p */
+  int hash_labels;       /* hash cliques by the graph's original labels when stored */
+  int64_t root_begin;    /* root sample: begin, end (-1 = all), stride */
+  int64_t root_end;
+  int64_t root_stride;
+  int include_isolated;  /* second-level runs: report isolated vertices */
+  int64_t collect_cap;   /* int64 words of the clique stream (0 = count only) */
+  int64_t capacity_bits; /* bitset capacity; |P| above it -> -4 (0 = 1024) */
+  double mem_fraction;   /* share of free HBM for per-worker scratch (0 -> 0.5) */
+} mce_run_config;
+
+typedef struct {
+  int64_t cliques;       /* maximal cliques */
+  int64_t nodes;         /* search-tree nodes (reference node accounting) */
+  uint64_t hash;         /* sum over cliques of mix64(sum mix64(label) + size*salt) */
+  int64_t max_size;
+  int64_t donations;
+  int64_t workers;       /* worker slots reported in worker_metrics */
+  int64_t launches;      /* enumeration kernels launched */
+  int64_t collect_len;   /* words the clique stream needed (may exceed collect_cap) */
+  int64_t hist[MCE_HIST_MAX]; /* hist[s] = maximal cliques of size s */
+} mce_run_result;
+
+/* Enumerate every maximal clique of a canonical, degeneracy-reordered graph
+ * (scheduler.py:441-492).  `collect` (host, collect_cap words) receives the
+ * clique stream [size, v0, v1, ...]...; `worker_metrics` (host, 4 int64 per
+ * worker: nodes, roots claimed, donations made, donations received). */
+int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collect,
+                  int64_t* worker_metrics, int64_t worker_metrics_cap, mce_run_result* out,
+                  void* stream);
+
+/* R-MAT edge generator on the device (input synthesis for the benchmarks):
+ * edges [start, start+count) of the counter-based stream of
+ * paper_2212_01473_b200/generate.py:rmat_edges, written as int64 pairs to a
+ * device buffer. */
+int mce_gen_rmat(int scale, int64_t start, int64_t count, uint64_t seed, int64_t* edges_dev,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,123 @@
+"""Clique sinks, subtree roots and the whole-graph enumerators
+(reference mce/bk.py).
+
+``CliqueSink`` and the root extractors are host-side data plumbing with the
+reference's exact semantics.  ``bk_pivot`` / ``bk_basic`` enumerate through
+the GPU engine (``scheduler.run``): the clique set of a graph does not
+depend on the traversal, so they return the reference's count and cliques.
+The brute-force ``oracle_enumerate`` of the reference is test
+infrastructure and lives in ``oracle/`` (not in the product).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, Iterator
+
+import numpy as np
+
+from paper_2212_01473_b200.graph import Graph
+
+
+class CliqueSink:
+    """Receives maximal cliques: always counts, optionally collects sorted
+    tuples up to ``collect_limit`` (reference bk.py:23-61)."""
+
+    __slots__ = ("collect_limit", "total", "collected")
+
+    def __init__(self, collect_limit: int | None = None) -> None:
+        self.collect_limit = collect_limit
+        self.total = 0
+        self.collected: list[tuple[int, ...]] = []
+
+    @classmethod
+    def counting(cls) -> "CliqueSink":
+        return cls(collect_limit=None)
+
+    @classmethod
+    def collecting(cls, limit: int = 1 << 20) -> "CliqueSink":
+        return cls(collect_limit=limit)
+
+    def report(self, vertices: Iterable[int]) -> None:
+        self.total += 1
+        if self.collect_limit is not None and len(self.collected) < self.collect_limit:
+            self.collected.append(tuple(sorted(int(v) for v in vertices)))
+
+    def merge(self, other: "CliqueSink") -> None:
+        self.total += other.total
+        if self.collect_limit is not None:
+            room = self.collect_limit - len(self.collected)
+            if room > 0:
+                self.collected.extend(other.collected[:room])
+
+    def clique_set(self) -> set[tuple[int, ...]]:
+        return set(self.collected)
+
+
+@dataclass(frozen=True)
+class RootTask:
+    """Seed state of one independent subtree (reference bk.py:64-76)."""
+
+    root_vertices: tuple[int, ...]
+    P: np.ndarray
+    X: np.ndarray
+    origin_index: int
+
+
+def first_level_root(g: Graph, v: int) -> RootTask:
+    """Per-vertex root: P = later neighbours, X = earlier (bk.py:188-192)."""
+    adj = g.neighbors(v)
+    cut = int(np.searchsorted(adj, v))
+    return RootTask((v,), adj[cut:].copy(), adj[:cut].copy(), origin_index=v)
+
+
+def first_level_roots(g: Graph) -> Iterator[RootTask]:
+    for v in range(g.num_vertices):
+        yield first_level_root(g, v)
+
+
+def second_level_root(g: Graph, edge_index: int) -> RootTask:
+    """Per-edge root: common neighbours after / before the later endpoint
+    (bk.py:200-206)."""
+    u, v = (int(a) for a in g.edges()[edge_index])
+    common = np.intersect1d(g.neighbors(u), g.neighbors(v), assume_unique=True)
+    cut = int(np.searchsorted(common, max(u, v)))
+    return RootTask((u, v), common[cut:].copy(), common[:cut].copy(), origin_index=edge_index)
+
+
+def second_level_roots(g: Graph) -> Iterator[RootTask]:
+    for e in range(len(g.edges())):
+        yield second_level_root(g, e)
+
+
+def _enumerate_whole_graph(g: Graph, sink: CliqueSink, metrics: dict | None) -> int:
+    from paper_2212_01473_b200.graph import preprocess
+    from paper_2212_01473_b200.scheduler import RunConfig, run
+
+    if g.num_vertices == 0:
+        if metrics is not None:
+            metrics["nodes"] = 0
+        return sink.total
+    g2, order, st = preprocess(g)
+    inner = CliqueSink(collect_limit=sink.collect_limit)
+    res = run(g2, st, RunConfig(workers=0), sink=inner)
+    inverse = np.argsort(order.position)
+    sink.total += inner.total
+    if sink.collect_limit is not None:
+        room = sink.collect_limit - len(sink.collected)
+        for c in inner.collected[:max(room, 0)]:
+            sink.collected.append(tuple(sorted(int(inverse[v]) for v in c)))
+    if metrics is not None:
+        metrics["nodes"] = res.nodes_total
+    return sink.total
+
+
+def bk_pivot(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
+    """All maximal cliques of ``g`` (reference bk.py:140-174) via the GPU
+    engine; cliques are reported in ``g``'s labels."""
+    return _enumerate_whole_graph(g, sink, metrics)
+
+
+def bk_basic(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
+    """Same clique set as reference bk.py:112-137 (the GPU engine always pivots)."""
+    return _enumerate_whole_graph(g, sink, metrics)

@@ -1,0 +1,48 @@
+// Shared device helpers and the device-resident graph layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MCE_CHECK(call)                                                          \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      mce_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,                   \
+                    cudaGetErrorString(_e));                                     \
+      return -1;                                                                 \
+    }                                                                            \
+  } while (0)
+
+void mce_set_error(const char* fmt, ...);
+
+// splitmix64 finaliser: the per-vertex term of the clique-set hash and the
+// counter-based RNG of the generators (identical on host and device).
+__host__ __device__ __forceinline__ uint64_t mce_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+#define MCE_SIZE_SALT 0xD1B54A32D192ED03ull
+
+// Device-resident canonical graph: symmetric CSR, rows strictly ascending.
+// `split[v]` indexes the first neighbour > v, so N-(v) = col[ro[v], split[v])
+// (earlier neighbours, the first-level X) and N+(v) = col[split[v], ro[v+1])
+// (later neighbours, the first-level P) -- the "CSR orientation".
+struct mce_graph {
+  int64_t n = 0;
+  int64_t nnz = 0;            // directed entries = 2m
+  int64_t* ro = nullptr;      // n + 1
+  int32_t* col = nullptr;     // nnz
+  int64_t* split = nullptr;   // n (lazily built)
+  int64_t* labels = nullptr;  // optional: original label of every vertex (set by reorder)
+  int64_t max_degree = 0;
+  int64_t max_later = 0;      // max |N+(v)|  (= degeneracy on a reordered graph)
+  int64_t max_earlier = 0;    // max |N-(v)|
+  int device = 0;
+};
+
+int mce_graph_build_split(mce_graph* g, cudaStream_t s);
+
+static inline int mce_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

@@ -1,0 +1,1074 @@
+// Maximal clique enumeration on the device: per-warp depth-first
+// Bron-Kerbosch with pivoting over independent subtrees, binary-encoded
+// induced subgraphs, the split X_P / X_X excluded-set representation and a
+// worker list through which busy warps donate branches to idle warps.
+//
+// Reference behaviour restated (file:line in /root/reference/pkg/src/mce):
+//   root tasks ............. bk.py:188-206           (first/second-level subtrees)
+//   induced rows ........... induced.py:58-98        (partial "ip" / full "ipx")
+//   pivot .................. bk.py:81-109            (max |N(c) & P| over P|X_P, ties to the
+//                                                     smallest id; X_X rows only if strictly
+//                                                     better, first in prefix order)
+//   traversal, node count .. scheduler.py:297-381
+//   X_X stable partition ... xsets.py:71-94
+//   donation conditions .... scheduler.py:346-355
+//   worker list protocol ... scheduler.py:99-165
+//   isolated vertices (l2) . scheduler.py:476-480
+//
+// The traversal tree (pivot choices, branch order, node accounting) is the
+// reference's exactly, so the node total is bit-identical for every worker
+// count and donation schedule.
+//
+// Layout.  One warp is one worker (the paper's thread block).  A bitset over
+// the root's P (|P| <= CAP = 32*W) is W 32-bit words held one word per lane
+// (lanes >= W hold 0).  Induced rows are stored transposed, rowsT[w][c] =
+// word w of row c, with column stride CAP+1 so both access patterns are
+// bank-conflict free: lane-per-candidate pivot scans read consecutive
+// columns, lane-per-word row loads read one column across words.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "mce_common.cuh"
+#include "mce_b200.h"
+
+namespace {
+
+constexpr int HIST_SMEM = 128;
+constexpr int HIST_MAX = MCE_HIST_MAX;
+constexpr unsigned FULLMASK = 0xffffffffu;
+
+struct WorkerListDev {
+  int lock;
+  int head;
+  int count;
+  int idle;
+  int in_flight;
+  int terminated;
+  int pad[2];
+};
+
+struct Mailbox {
+  int64_t origin;   // root task the branch belongs to
+  int32_t rlen;     // R path length, written into the receiver's rpath
+  int32_t nxx;      // live X_X tokens, written into the receiver's xx
+  int32_t has_task;
+  int32_t pad;
+  uint32_t P[32];
+  uint32_t XP[32];
+};
+
+struct EnumArgs {
+  int64_t n;
+  const int64_t* ro;
+  const int32_t* col;
+  const int64_t* split;
+  const uint64_t* vhash;  // mix64(label(v))
+  const int64_t* roots;   // l1: vertex, l2: (u << 32) | v
+  int64_t num_roots;
+  unsigned long long* root_counter;
+  int roots_mode;
+  int num_workers;
+  int64_t xcap;
+  int levels;
+  // per-worker scratch
+  uint32_t* rows_g;
+  int32_t* plist_g;
+  uint32_t* xrows;
+  int32_t* xlist;
+  int32_t* xx;
+  int32_t* xtmp;
+  uint32_t* stack;
+  int32_t* lpx;
+  int32_t* rpath;
+  uint64_t* hsum;
+  // outputs
+  unsigned long long* g_acc;   // 0 cliques, 1 hash, 2 nodes, 3 donations, 4 max size
+  unsigned long long* g_hist;  // HIST_MAX
+  long long* w_metrics;        // per worker: nodes, roots, donations made, received
+  int64_t* collect;
+  int64_t collect_cap;
+  unsigned long long* collect_len;
+  // worker list
+  WorkerListDev* wl;
+  int* wl_ring;
+  int* wl_wake;
+  Mailbox* mbox;
+  int worker_list_on;
+  int min_p;
+};
+
+__device__ __forceinline__ int bsearch_i32(const int32_t* a, int len, int32_t key) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return (lo < len && a[lo] == key) ? lo : -1;
+}
+
+__device__ __forceinline__ bool contains_range(const int32_t* __restrict__ col, int64_t lo,
+                                               int64_t hi, int32_t key) {
+  int64_t end = hi;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (col[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo < end && col[lo] == key;
+}
+
+__device__ __forceinline__ void spin_lock(int* l) {
+  while (atomicCAS(l, 0, 1) != 0) __nanosleep(32);
+  __threadfence();
+}
+
+__device__ __forceinline__ void spin_unlock(int* l) {
+  __threadfence();
+  atomicExch(l, 0);
+}
+
+template <int W, bool FULL, bool ROWS_SMEM>
+struct Worker {
+  static constexpr int CAP = 32 * W;
+  static constexpr int CAPP = CAP + 1;
+
+  const EnumArgs& a;
+  const int lane;
+  const int wid;
+  uint32_t* rowsT;
+  int32_t* plist;
+  uint32_t* sP;
+  unsigned long long* s_hist;
+  uint32_t* xrowsT;
+  int32_t* xlist_buf;
+  int32_t* xx;
+  int32_t* xtmp;
+  uint32_t* stk;
+  int32_t* lpx;
+  int32_t* rpath;
+  uint64_t* hsum;
+  const int32_t* root_x;
+  int np = 0, nx = 0;
+  int64_t origin = 0;
+  // metrics (uniform across the warp)
+  long long nodes = 0, roots_claimed = 0, don_made = 0, don_recv = 0;
+  unsigned long long cliques = 0, hash = 0, max_size = 0;
+  bool phase2_seen = false;
+
+  __device__ Worker(const EnumArgs& args, int lane_, int wid_, uint32_t* smem_rows,
+                    int32_t* smem_plist, uint32_t* smem_p, unsigned long long* smem_hist)
+      : a(args), lane(lane_), wid(wid_), sP(smem_p), s_hist(smem_hist) {
+    if (ROWS_SMEM) {
+      rowsT = smem_rows;
+      plist = smem_plist;
+    } else {
+      rowsT = a.rows_g + (size_t)wid * W * CAPP;
+      plist = a.plist_g + (size_t)wid * CAP;
+    }
+    xrowsT = FULL ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
+    xlist_buf = a.xlist ? a.xlist + (size_t)wid * a.xcap : nullptr;
+    xx = a.xx + (size_t)wid * a.xcap;
+    xtmp = a.xtmp + (size_t)wid * a.xcap;
+    stk = a.stack + (size_t)wid * a.levels * 3 * W;
+    lpx = a.lpx + (size_t)wid * a.levels;
+    rpath = a.rpath + (size_t)wid * (a.levels + 2);
+    hsum = a.hsum + (size_t)wid * (a.levels + 2);
+  }
+
+  __device__ __forceinline__ uint32_t row_word(int c, int w) const { return rowsT[w * CAPP + c]; }
+
+  // ---------------------------------------------------------------- build
+  // Fill plist / root_x / rows (and X rows) for root `r`; returns R0 length.
+  __device__ int build(int64_t r) {
+    const int32_t* col = a.col;
+    int nr;
+    if (a.roots_mode == 1) {
+      const int64_t v = r;
+      const int64_t s = a.split[v];
+      np = (int)(a.ro[v + 1] - s);
+      nx = (int)(s - a.ro[v]);
+      for (int i = lane; i < np; i += 32) plist[i] = col[s + i];
+      root_x = col + a.ro[v];
+      if (lane == 0) rpath[0] = (int32_t)v;
+      nr = 1;
+    } else {
+      const int64_t u = r >> 32, v = r & 0xffffffffll;
+      // P = N+(u) & N+(v), X = N(u) & N-(v), both ascending (bk.py:200-206)
+      np = 0;
+      const int64_t ps = a.split[v], pe = a.ro[v + 1];
+      const int64_t us = a.split[u], ue = a.ro[u + 1];
+      for (int64_t base = ps; base < pe; base += 32) {
+        int64_t e = base + lane;
+        bool in = false;
+        int32_t w = 0;
+        if (e < pe) {
+          w = col[e];
+          in = contains_range(col, us, ue, w);
+        }
+        unsigned m = __ballot_sync(FULLMASK, in);
+        if (in) plist[np + __popc(m & ((1u << lane) - 1))] = w;
+        np += __popc(m);
+      }
+      nx = 0;
+      const int64_t xs = a.ro[v], xe = a.split[v];
+      const int64_t u0 = a.ro[u];
+      for (int64_t base = xs; base < xe; base += 32) {
+        int64_t e = base + lane;
+        bool in = false;
+        int32_t w = 0;
+        if (e < xe) {
+          w = col[e];
+          in = contains_range(col, u0, ue, w);
+        }
+        unsigned m = __ballot_sync(FULLMASK, in);
+        if (in) xlist_buf[nx + __popc(m & ((1u << lane) - 1))] = w;
+        nx += __popc(m);
+      }
+      root_x = xlist_buf;
+      if (lane == 0) {
+        rpath[0] = (int32_t)u;
+        rpath[1] = (int32_t)v;
+      }
+      nr = 2;
+    }
+    origin = r;
+    __syncwarp();
+    if (np == 0) return nr;
+    // P rows (induced.py:80-87): each P-P edge (a_i, b) with b in N+(a_i)
+    for (int w = 0; w < W; ++w)
+      for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
+    __syncwarp();
+    for (int i = 0; i < np; ++i) {
+      const int32_t ai = plist[i];
+      const int64_t lo = a.split[ai], hi = a.ro[ai + 1];
+      for (int64_t e = lo + lane; e < hi; e += 32) {
+        int j = bsearch_i32(plist, np, col[e]);
+        if (j >= 0) {
+          atomicOr(&rowsT[(j >> 5) * CAPP + i], 1u << (j & 31));
+          atomicOr(&rowsT[(i >> 5) * CAPP + j], 1u << (i & 31));
+        }
+      }
+    }
+    if (FULL) {
+      // X rows (induced.py:90-98): X member x is earlier than every P vertex,
+      // so its P-neighbours are N+(x) & P.  Lane t owns column t.
+      for (int t = lane; t < nx; t += 32) {
+        for (int w = 0; w < W; ++w) xrowsT[(size_t)w * a.xcap + t] = 0;
+        const int32_t x = root_x[t];
+        const int64_t lo = a.split[x], hi = a.ro[x + 1];
+        for (int64_t e = lo; e < hi; ++e) {
+          int j = bsearch_i32(plist, np, col[e]);
+          if (j >= 0) xrowsT[(size_t)(j >> 5) * a.xcap + t] |= 1u << (j & 31);
+        }
+      }
+    }
+    __syncwarp();
+    return nr;
+  }
+
+  // ---------------------------------------------------------------- pieces
+  __device__ __forceinline__ bool xx_adjacent(int32_t t, int v, int32_t gv) const {
+    if (FULL) return (xrowsT[(size_t)(v >> 5) * a.xcap + t] >> (v & 31)) & 1u;
+    const int32_t x = root_x[t];
+    return contains_range(a.col, a.split[x], a.ro[x + 1], gv);
+  }
+
+  __device__ bool xx_any_adjacent(int v, int32_t gv, int live) const {
+    for (int base = 0; base < live; base += 32) {
+      int i = base + lane;
+      bool hit = (i < live) && xx_adjacent(xx[i], v, gv);
+      if (__any_sync(FULLMASK, hit)) return true;
+    }
+    return false;
+  }
+
+  // stable partition of xx[0, live) by adjacency to v (xsets.py:71-94)
+  __device__ int partition(int v, int32_t gv, int live) {
+    int kept = 0, dropped = 0;
+    const unsigned lt = (1u << lane) - 1;
+    for (int base = 0; base < live; base += 32) {
+      int i = base + lane;
+      bool valid = i < live;
+      int32_t t = valid ? xx[i] : 0;
+      bool keep = valid && xx_adjacent(t, v, gv);
+      unsigned km = __ballot_sync(FULLMASK, keep);
+      unsigned dm = __ballot_sync(FULLMASK, valid && !keep);
+      if (keep) xx[kept + __popc(km & lt)] = t;
+      else if (valid) xtmp[dropped + __popc(dm & lt)] = t;
+      kept += __popc(km);
+      dropped += __popc(dm);
+    }
+    __syncwarp();
+    for (int i = lane; i < dropped; i += 32) xx[kept + i] = xtmp[i];
+    __syncwarp();
+    return kept;
+  }
+
+  // pivot (bk.py:81-109); returns this lane's word of P - N(pivot)
+  __device__ uint32_t pivot_branches(uint32_t P, uint32_t XP, int live) {
+    if (lane < W) sP[lane] = P;
+    __syncwarp();
+    const uint32_t C = P | XP;
+    const unsigned cmask = __ballot_sync(FULLMASK, C != 0);
+    const unsigned pmask = __ballot_sync(FULLMASK, P != 0);
+    int best = -1, bestc = 0x7fffffff;
+    for (unsigned cm = cmask; cm; cm &= cm - 1) {
+      const int w = __ffs(cm) - 1;
+      const uint32_t Cw = __shfl_sync(FULLMASK, C, w);
+      const int c = w * 32 + lane;
+      int cnt = 0;
+      for (unsigned pm = pmask; pm; pm &= pm - 1) {
+        const int j = __ffs(pm) - 1;
+        cnt += __popc(rowsT[j * CAPP + c] & sP[j]);
+      }
+      if (((Cw >> lane) & 1u) && cnt > best) {
+        best = cnt;
+        bestc = c;
+      }
+    }
+    const int m = (int)__reduce_max_sync(FULLMASK, (unsigned)(best + 1)) - 1;
+    const int pc = __reduce_min_sync(FULLMASK, best == m ? bestc : 0x7fffffff);
+    uint32_t prow;
+    bool use_local = true;
+    if (FULL && live > 0) {
+      int xb = -1, xpos = 0x7fffffff;
+      for (int base = 0; base < live; base += 32) {
+        const int i = base + lane;
+        if (i < live) {
+          const int32_t t = xx[i];
+          int cnt = 0;
+          for (unsigned pm = pmask; pm; pm &= pm - 1) {
+            const int j = __ffs(pm) - 1;
+            cnt += __popc(xrowsT[(size_t)j * a.xcap + t] & sP[j]);
+          }
+          if (cnt > xb) {
+            xb = cnt;
+            xpos = i;
+          }
+        }
+      }
+      const int xm = (int)__reduce_max_sync(FULLMASK, (unsigned)(xb + 1)) - 1;
+      if (xm > m) {
+        const int pos = __reduce_min_sync(FULLMASK, xb == xm ? xpos : 0x7fffffff);
+        const int32_t t = xx[pos];
+        prow = (lane < W) ? xrowsT[(size_t)lane * a.xcap + t] : 0u;
+        use_local = false;
+      }
+    }
+    if (use_local) prow = (lane < W) ? row_word(pc, lane) : 0u;
+    __syncwarp();
+    return P & ~prow;
+  }
+
+  __device__ void report(int size, uint64_t hs) {
+    if (lane == 0) {
+      cliques++;
+      hash += mce_mix64(hs + (uint64_t)size * MCE_SIZE_SALT);
+      if ((unsigned long long)size > max_size) max_size = size;
+      if (size < HIST_SMEM) atomicAdd(&s_hist[size], 1ull);
+      else atomicAdd(&a.g_hist[size < HIST_MAX ? size : HIST_MAX - 1], 1ull);
+    }
+    if (a.collect_cap > 0) {
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(a.collect_len, (unsigned long long)(size + 1));
+      pos = __shfl_sync(FULLMASK, pos, 0);
+      __syncwarp();
+      if (pos + size + 1 <= (unsigned long long)a.collect_cap) {
+        if (lane == 0) a.collect[pos] = size;
+        for (int i = lane; i < size; i += 32) a.collect[pos + 1 + i] = rpath[i];
+      }
+    }
+  }
+
+  __device__ bool phase2() {
+    if (!phase2_seen) {
+      unsigned long long c = *(volatile unsigned long long*)a.root_counter;
+      phase2_seen = c >= (unsigned long long)a.num_roots;
+    }
+    return phase2_seen;
+  }
+
+  // donate the branch (v, childP, childXP) to an idle worker (scheduler.py:417-438)
+  __device__ bool try_donate(uint32_t childP, uint32_t childXP, int v, int32_t gv, int live,
+                             int rlen) {
+    int rid = -1;
+    if (lane == 0) {
+      WorkerListDev* wl = a.wl;
+      if (*(volatile int*)&wl->count > 0) {
+        spin_lock(&wl->lock);
+        if (wl->count > 0 && !wl->terminated) {
+          rid = a.wl_ring[wl->head];
+          wl->head = (wl->head + 1) % a.num_workers;
+          wl->count--;
+          wl->in_flight++;
+        }
+        spin_unlock(&wl->lock);
+      }
+    }
+    rid = __shfl_sync(FULLMASK, rid, 0);
+    if (rid < 0) return false;
+    Mailbox* mb = a.mbox + rid;
+    int32_t* rx = a.xx + (size_t)rid * a.xcap;
+    int32_t* rr = a.rpath + (size_t)rid * (a.levels + 2);
+    // receiver's X_X: the live tokens adjacent to v, in prefix order
+    int k = 0;
+    const unsigned lt = (1u << lane) - 1;
+    for (int base = 0; base < live; base += 32) {
+      int i = base + lane;
+      bool keep = (i < live) && xx_adjacent(xx[i], v, gv);
+      unsigned km = __ballot_sync(FULLMASK, keep);
+      if (keep) rx[k + __popc(km & lt)] = xx[i];
+      k += __popc(km);
+    }
+    for (int i = lane; i < rlen; i += 32) rr[i] = rpath[i];
+    if (lane == 0) {
+      rr[rlen] = gv;
+      mb->origin = origin;
+      mb->rlen = rlen + 1;
+      mb->nxx = k;
+      mb->has_task = 1;
+    }
+    mb->P[lane] = childP;
+    mb->XP[lane] = childXP;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicExch(&a.wl_wake[rid], 1);
+    don_made++;
+    return true;
+  }
+
+  // park on the worker list until donated to (true) or terminated (false)
+  __device__ bool park() {
+    int got = 0;
+    if (lane == 0) {
+      WorkerListDev* wl = a.wl;
+      bool done = false;
+      spin_lock(&wl->lock);
+      if (wl->terminated) {
+        done = true;
+      } else if (wl->idle + 1 == a.num_workers && wl->in_flight == 0) {
+        wl->terminated = 1;
+        for (int i = 0; i < a.num_workers; ++i) atomicExch(&a.wl_wake[i], 1);
+        done = true;
+      } else {
+        wl->idle++;
+        a.wl_ring[(wl->head + wl->count) % a.num_workers] = wid;
+        wl->count++;
+      }
+      spin_unlock(&wl->lock);
+      if (!done) {
+        unsigned ns = 64;
+        while (*(volatile int*)&a.wl_wake[wid] == 0) {
+          __nanosleep(ns);
+          ns = ns < 8192 ? ns * 2 : ns;
+        }
+        __threadfence();
+        spin_lock(&wl->lock);
+        a.wl_wake[wid] = 0;
+        Mailbox* mb = a.mbox + wid;
+        got = mb->has_task;
+        mb->has_task = 0;
+        wl->idle--;
+        if (got) wl->in_flight--;
+        spin_unlock(&wl->lock);
+      }
+    }
+    got = __shfl_sync(FULLMASK, got, 0);
+    __threadfence();
+    return got != 0;
+  }
+
+  // ---------------------------------------------------------------- DFS
+  // Traverse from the level-0 state (P, XP, xx[0, nxx), rpath[0, rlen)).
+  __device__ void traverse(uint32_t P, uint32_t XP, int nxx, int rlen) {
+    uint64_t hs = 0;
+    for (int i = 0; i < rlen; ++i) hs += a.vhash[rpath[i]];
+    const bool p_empty = __ballot_sync(FULLMASK, P != 0) == 0;
+    if (p_empty) {  // scheduler.py:300-304
+      nodes++;
+      const bool x_empty = __ballot_sync(FULLMASK, XP != 0) == 0 && nxx == 0;
+      if (x_empty) report(rlen, hs);
+      return;
+    }
+    int depth = 0;
+    int below = 0;  // frozen frames with branches left (scheduler.py:348)
+    if (lane == 0) {
+      lpx[0] = nxx;
+      hsum[rlen] = hs;
+    }
+    int live = nxx;
+    nodes++;
+    uint32_t BR = pivot_branches(P, XP, live);
+    for (;;) {
+      const unsigned bm = __ballot_sync(FULLMASK, BR != 0);
+      if (bm == 0) {
+        if (depth == 0) break;
+        depth--;
+        rlen--;
+        if (lane < W) {
+          const uint32_t* f = stk + (size_t)depth * 3 * W;
+          P = f[lane];
+          XP = f[W + lane];
+          BR = f[2 * W + lane];
+        }
+        if (__ballot_sync(FULLMASK, BR != 0)) below--;
+        live = lpx[depth];
+        continue;
+      }
+      const int fl = __ffs(bm) - 1;
+      const uint32_t word = __shfl_sync(FULLMASK, BR, fl);
+      const int b = __ffs(word) - 1;
+      const int v = fl * 32 + b;
+      if (lane == fl) {
+        const uint32_t bit = 1u << b;
+        BR &= ~bit;
+        P &= ~bit;
+        XP |= bit;
+      }
+      const uint32_t rowv = (lane < W) ? row_word(v, lane) : 0u;
+      const uint32_t childP = P & rowv;
+      const int cpop = __reduce_add_sync(FULLMASK, __popc(childP));
+      const int32_t gv = plist[v];
+      if (a.worker_list_on && cpop >= a.min_p && below > 0 &&
+          __ballot_sync(FULLMASK, BR != 0) != 0 && phase2()) {
+        if (try_donate(childP, XP & rowv, v, gv, live, rlen)) continue;
+      }
+      if (cpop == 0) {  // scheduler.py:358-369
+        nodes++;
+        bool hit = __ballot_sync(FULLMASK, (XP & rowv) != 0) != 0;
+        if (!hit) hit = xx_any_adjacent(v, gv, live);
+        if (!hit) {
+          if (lane == 0) rpath[rlen] = gv;
+          __syncwarp();
+          report(rlen + 1, hsum[rlen] + a.vhash[gv]);
+        }
+        continue;
+      }
+      const int kept = partition(v, gv, live);
+      if (lane < W) {
+        uint32_t* f = stk + (size_t)depth * 3 * W;
+        f[lane] = P;
+        f[W + lane] = XP;
+        f[2 * W + lane] = BR;
+      }
+      if (__ballot_sync(FULLMASK, BR != 0)) below++;
+      depth++;
+      live = kept;
+      XP &= rowv;
+      P = childP;
+      if (lane == 0) {
+        lpx[depth] = kept;
+        rpath[rlen] = gv;
+        hsum[rlen + 1] = hsum[rlen] + a.vhash[gv];
+      }
+      rlen++;
+      nodes++;
+      __syncwarp();
+      BR = pivot_branches(P, XP, live);
+    }
+  }
+
+  __device__ void run_root(int64_t r) {
+    const int nr = build(r);
+    uint32_t P = 0;
+    if (lane < W) {
+      const int lo = lane * 32;
+      if (np >= lo + 32) P = 0xffffffffu;
+      else if (np > lo) P = (1u << (np - lo)) - 1u;
+    }
+    for (int t = lane; t < nx; t += 32) xx[t] = t;
+    __syncwarp();
+    traverse(P, 0u, nx, nr);
+  }
+
+  __device__ void run_donated() {
+    const Mailbox* mb = a.mbox + wid;
+    const int64_t r = mb->origin;
+    const int rlen = mb->rlen;
+    const int nxx = mb->nxx;
+    const uint32_t P = (lane < W) ? mb->P[lane] : 0u;
+    const uint32_t XP = (lane < W) ? mb->XP[lane] : 0u;
+    // rebuild the origin's induced rows; rpath/xx were written by the donor,
+    // so save the donated path across build()'s R0 write
+    int32_t keep0 = 0, keep1 = 0;
+    if (lane == 0) {
+      keep0 = rpath[0];
+      keep1 = rpath[1];
+    }
+    build(r);
+    if (lane == 0) {
+      rpath[0] = keep0;
+      rpath[1] = keep1;
+    }
+    __syncwarp();
+    traverse(P, XP, nxx, rlen);
+  }
+};
+
+template <int W, bool FULL, bool ROWS_SMEM, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
+  constexpr int CAP = 32 * W;
+  constexpr int CAPP = CAP + 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem);
+  uint32_t* s_p = reinterpret_cast<uint32_t*>(s_hist + HIST_SMEM);
+  uint32_t* s_rows = s_p + WARPS * 32;
+  int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? WARPS * W * CAPP : 0));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  const int wid = blockIdx.x * WARPS + warp;
+  if (wid < a.num_workers) {
+    Worker<W, FULL, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
+                                  s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + warp * 32,
+                                  s_hist);
+    for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-260)
+      unsigned long long idx = 0;
+      if (lane == 0) idx = atomicAdd(a.root_counter, 1ull);
+      idx = __shfl_sync(FULLMASK, idx, 0);
+      if (idx >= (unsigned long long)a.num_roots) break;
+      wk.roots_claimed++;
+      wk.run_root(a.roots[idx]);
+    }
+    if (a.worker_list_on) {  // phase 2: park, receive donated branches
+      while (wk.park()) {
+        wk.don_recv++;
+        wk.run_donated();
+      }
+    }
+    if (lane == 0) {
+      atomicAdd(&a.g_acc[0], wk.cliques);
+      atomicAdd(&a.g_acc[1], wk.hash);
+      atomicAdd(&a.g_acc[2], (unsigned long long)wk.nodes);
+      atomicAdd(&a.g_acc[3], (unsigned long long)wk.don_made);
+      atomicMax(&a.g_acc[4], wk.max_size);
+      long long* m = a.w_metrics + (size_t)wid * 4;
+      m[0] += wk.nodes;
+      m[1] += wk.roots_claimed;
+      m[2] += wk.don_made;
+      m[3] += wk.don_recv;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&a.g_hist[i], s_hist[i]);
+}
+
+// ------------------------------------------------------------ root prep
+
+// l1 roots: |P| = |N+(v)|; l2 roots: edges (u < v) with bound |N+(v)|
+__global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
+                            const int32_t* __restrict__ col, const int64_t* __restrict__ eoff,
+                            int64_t n, int roots_mode, int64_t begin, int64_t stride,
+                            int64_t count, uint32_t* __restrict__ keys,
+                            int64_t* __restrict__ roots) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = begin + i * stride;
+    int64_t p;
+    if (roots_mode == 1) {
+      p = ro[r + 1] - split[r];
+      roots[i] = r;
+    } else {
+      int64_t lo = 0, hi = n;  // largest u with eoff[u] <= r
+      while (hi - lo > 1) {
+        int64_t mid = (lo + hi) >> 1;
+        if (eoff[mid] <= r) lo = mid; else hi = mid;
+      }
+      const int64_t u = lo;
+      const int64_t v = col[split[u] + (r - eoff[u])];
+      p = ro[v + 1] - split[v];
+      roots[i] = (u << 32) | v;
+    }
+    // ascending key = descending |P| (heavy subtrees first); zero-P first-level
+    // roots get the largest key and are counted without a worker
+    keys[i] = (roots_mode == 1 && p == 0) ? 0xffffffffu : (uint32_t)(0x7fffffff - p);
+  }
+}
+
+__global__ void k_later_count(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
+                              int64_t n, int64_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = ro[v + 1] - split[v];
+}
+
+__global__ void k_vhash(const int64_t* __restrict__ labels, int64_t n, uint64_t* __restrict__ vh) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    vh[v] = mce_mix64((uint64_t)(labels ? labels[v] : v));
+}
+
+// first-level roots with P empty (scheduler.py:300-304) and, for second-level
+// runs, isolated vertices (scheduler.py:476-480): one node / one singleton each
+__global__ void k_trivial_roots(const int64_t* __restrict__ roots, int64_t count,
+                                const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
+                                const uint64_t* __restrict__ vhash,
+                                unsigned long long* __restrict__ acc,
+                                unsigned long long* __restrict__ hist, int64_t* collect,
+                                int64_t collect_cap, unsigned long long* collect_len) {
+  unsigned long long c = 0, h = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = roots[i];
+    if (ro[v + 1] == ro[v]) {
+      c++;
+      h += mce_mix64(vhash[v] + MCE_SIZE_SALT);
+      if (collect_cap > 0) {
+        unsigned long long pos = atomicAdd(collect_len, 2ull);
+        if (pos + 2 <= (unsigned long long)collect_cap) {
+          collect[pos] = 1;
+          collect[pos + 1] = v;
+        }
+      }
+    }
+  }
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage t1, t2;
+  unsigned long long cs = BR(t1).Sum(c);
+  unsigned long long hsum = BR(t2).Sum(h);
+  if (threadIdx.x == 0) {
+    if (cs) {
+      atomicAdd(&acc[0], cs);
+      atomicAdd(&acc[1], hsum);
+      atomicAdd(&hist[1], cs);
+      atomicMax(&acc[4], 1ull);
+    }
+  }
+}
+
+__global__ void k_isolated(int64_t n, const int64_t* __restrict__ ro, int64_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = v;
+}
+
+int grid_for(int64_t work, int threads = 256) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)g;
+}
+
+template <typename T>
+int dalloc(T** p, size_t count, cudaStream_t s) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  MCE_CHECK(cudaMallocAsync((void**)p, count * sizeof(T), s));
+  return 0;
+}
+
+struct ClassPlan {
+  int W;
+  int64_t begin, count;  // slice of the sorted root list
+};
+
+template <int W, bool FULL, bool ROWS_SMEM, int WARPS>
+int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cudaStream_t s,
+                 int64_t* launches, size_t mem_budget) {
+  constexpr int CAP = 32 * W;
+  constexpr int CAPP = CAP + 1;
+  auto kern = k_enumerate<W, FULL, ROWS_SMEM, WARPS>;
+  size_t smem = HIST_SMEM * sizeof(unsigned long long) + WARPS * 32 * sizeof(uint32_t) +
+                (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
+  MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
+  if (per_sm < 1) {
+    mce_set_error("enumerate kernel W=%d does not fit on an SM", W);
+    return -3;
+  }
+  // every worker must be co-resident: idle workers spin until woken
+  int64_t resident = (int64_t)per_sm * sms * WARPS;
+  const int64_t levels = CAP + 3;
+  const int64_t xcap = std::max<int64_t>(args.xcap, 1);
+  size_t per_worker = sizeof(uint32_t) * (size_t)(levels * 3 * W) + sizeof(int32_t) * levels +
+                      (sizeof(int32_t) + sizeof(uint64_t)) * (levels + 2) +
+                      sizeof(int32_t) * 2 * xcap + sizeof(Mailbox) + sizeof(int) * 2 +
+                      sizeof(long long) * 4 +
+                      (FULL ? sizeof(uint32_t) * (size_t)W * xcap : 0) +
+                      (args.roots_mode == 2 ? sizeof(int32_t) * xcap : 0) +
+                      (ROWS_SMEM ? 0 : sizeof(uint32_t) * (size_t)(W * CAPP + CAP));
+  int64_t by_mem = std::max<int64_t>(1, (int64_t)(mem_budget / per_worker));
+  int64_t workers = requested_workers > 0 ? requested_workers : resident;
+  workers = std::min<int64_t>(workers, resident);
+  workers = std::min<int64_t>(workers, by_mem);
+  if (requested_workers <= 0) workers = std::min<int64_t>(workers, std::max<int64_t>(args.num_roots, 1) + resident / 4);
+  workers = std::max<int64_t>(workers, 1);
+  args.num_workers = (int)workers;
+  args.levels = (int)levels;
+  args.xcap = xcap;
+  *workers_used = std::max<int64_t>(*workers_used, workers);
+  std::vector<void*> owned;
+  auto get = [&](auto** p, size_t count) -> int {
+    if (dalloc(p, count, s)) return -1;
+    owned.push_back((void*)*p);
+    return 0;
+  };
+  if (get(&args.stack, (size_t)workers * levels * 3 * W) || get(&args.lpx, (size_t)workers * levels) ||
+      get(&args.rpath, (size_t)workers * (levels + 2)) || get(&args.hsum, (size_t)workers * (levels + 2)) ||
+      get(&args.xx, (size_t)workers * xcap) || get(&args.xtmp, (size_t)workers * xcap) ||
+      get(&args.mbox, (size_t)workers) || get(&args.wl_ring, (size_t)workers) ||
+      get(&args.wl_wake, (size_t)workers) || get(&args.wl, 1) ||
+      get(&args.root_counter, 1))
+    return -1;
+  args.xrows = nullptr;
+  args.xlist = nullptr;
+  args.rows_g = nullptr;
+  args.plist_g = nullptr;
+  if (FULL && get(&args.xrows, (size_t)workers * W * xcap)) return -1;
+  if (args.roots_mode == 2 && get(&args.xlist, (size_t)workers * xcap)) return -1;
+  if (!ROWS_SMEM && (get(&args.rows_g, (size_t)workers * W * CAPP) ||
+                     get(&args.plist_g, (size_t)workers * CAP)))
+    return -1;
+  MCE_CHECK(cudaMemsetAsync(args.wl, 0, sizeof(WorkerListDev), s));
+  MCE_CHECK(cudaMemsetAsync(args.wl_wake, 0, sizeof(int) * workers, s));
+  MCE_CHECK(cudaMemsetAsync(args.mbox, 0, sizeof(Mailbox) * workers, s));
+  MCE_CHECK(cudaMemsetAsync(args.root_counter, 0, sizeof(unsigned long long), s));
+  const int grid = (int)((workers + WARPS - 1) / WARPS);
+  kern<<<grid, WARPS * 32, smem, s>>>(args);
+  MCE_CHECK(cudaGetLastError());
+  (*launches)++;
+  for (void* p : owned) cudaFreeAsync(p, s);
+  return 0;
+}
+
+template <bool FULL>
+int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, int64_t* launches,
+             size_t budget) {
+  switch (W) {
+    case 1: return launch_class<1, FULL, true, 8>(args, workers, used, s, launches, budget);
+    case 2: return launch_class<2, FULL, true, 8>(args, workers, used, s, launches, budget);
+    case 4: return launch_class<4, FULL, true, 8>(args, workers, used, s, launches, budget);
+    case 8: return launch_class<8, FULL, true, 4>(args, workers, used, s, launches, budget);
+    case 16: return launch_class<16, FULL, true, 2>(args, workers, used, s, launches, budget);
+    case 32: return launch_class<32, FULL, false, 4>(args, workers, used, s, launches, budget);
+  }
+  mce_set_error("unsupported bitset width %d", W);
+  return -3;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collect,
+                  int64_t* worker_metrics, int64_t worker_metrics_cap, mce_run_result* out,
+                  void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  memset(out, 0, sizeof(*out));
+  if (cfg->roots != 1 && cfg->roots != 2) {
+    mce_set_error("roots must be 1 (l1) or 2 (l2)");
+    return -2;
+  }
+  const int64_t n = g->n;
+  if (n == 0) return 0;
+  std::vector<void*> owned;
+  auto get = [&](auto** p, size_t count) -> int {
+    if (dalloc(p, count, s)) return -1;
+    owned.push_back((void*)*p);
+    return 0;
+  };
+  auto cleanup = [&]() {
+    for (void* p : owned) cudaFreeAsync(p, s);
+    owned.clear();
+  };
+  // --- root list ---------------------------------------------------------
+  int64_t* eoff = nullptr;
+  int64_t total_roots = n;
+  if (cfg->roots == 2) {
+    int64_t* later = nullptr;
+    if (get(&later, n) || get(&eoff, n + 1)) return -1;
+    k_later_count<<<grid_for(n), 256, 0, s>>>(g->ro, g->split, n, later);
+    MCE_CHECK(cudaMemsetAsync(eoff, 0, sizeof(int64_t), s));
+    size_t tb = 0;
+    MCE_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, later, eoff + 1, n, s));
+    void* tmp = nullptr;
+    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    MCE_CHECK(cub::DeviceScan::InclusiveSum(tmp, tb, later, eoff + 1, n, s));
+    cudaFreeAsync(tmp, s);
+    MCE_CHECK(cudaMemcpyAsync(&total_roots, eoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    MCE_CHECK(cudaStreamSynchronize(s));
+  }
+  int64_t begin = std::max<int64_t>(cfg->root_begin, 0);
+  int64_t end = (cfg->root_end < 0 || cfg->root_end > total_roots) ? total_roots : cfg->root_end;
+  int64_t stride = cfg->root_stride > 0 ? cfg->root_stride : 1;
+  int64_t count = end > begin ? (end - begin + stride - 1) / stride : 0;
+
+  uint64_t* vhash = nullptr;
+  unsigned long long *acc = nullptr, *hist = nullptr, *collect_len = nullptr;
+  long long* wmet = nullptr;
+  int64_t* d_collect = nullptr;
+  if (get(&vhash, n) || get(&acc, 8) || get(&hist, HIST_MAX) || get(&collect_len, 1)) {
+    cleanup();
+    return -1;
+  }
+  k_vhash<<<grid_for(n), 256, 0, s>>>(cfg->hash_labels ? g->labels : nullptr, n, vhash);
+  MCE_CHECK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), s));
+  MCE_CHECK(cudaMemsetAsync(hist, 0, HIST_MAX * sizeof(unsigned long long), s));
+  MCE_CHECK(cudaMemsetAsync(collect_len, 0, sizeof(unsigned long long), s));
+  if (cfg->collect_cap > 0 && get(&d_collect, cfg->collect_cap)) {
+    cleanup();
+    return -1;
+  }
+
+  int64_t max_workers_slots = 0;
+  int64_t launches = 0;
+  int64_t trivial_nodes = 0;
+  int64_t workers_used = 0;
+  if (count > 0) {
+    uint32_t *keys = nullptr, *keys2 = nullptr;
+    int64_t *roots = nullptr, *roots2 = nullptr;
+    if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count)) {
+      cleanup();
+      return -1;
+    }
+    k_root_keys<<<grid_for(count), 256, 0, s>>>(g->ro, g->split, g->col, eoff, n, cfg->roots,
+                                                 begin, stride, count, keys, roots);
+    MCE_CHECK(cudaGetLastError());
+    cub::DoubleBuffer<uint32_t> dk(keys, keys2);
+    cub::DoubleBuffer<int64_t> dv(roots, roots2);
+    size_t tb = 0;
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, count, 0, 32, s));
+    void* tmp = nullptr;
+    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 32, s));
+    cudaFreeAsync(tmp, s);
+    std::vector<uint32_t> hk(count);
+    MCE_CHECK(cudaMemcpyAsync(hk.data(), dk.Current(), sizeof(uint32_t) * count,
+                              cudaMemcpyDeviceToHost, s));
+    MCE_CHECK(cudaStreamSynchronize(s));
+    const int64_t* sorted_roots = dv.Current();
+    // class slices: keys ascending == |P| descending
+    auto pofkey = [](uint32_t k) -> int64_t {
+      return k == 0xffffffffu ? -1 : (int64_t)0x7fffffff - (int64_t)k;
+    };
+    const int64_t cap_limit = cfg->capacity_bits > 0 ? cfg->capacity_bits : 1024;
+    if (pofkey(hk[0]) > std::min<int64_t>(cap_limit, 1024)) {
+      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld",
+                    (long long)pofkey(hk[0]), (long long)std::min<int64_t>(cap_limit, 1024));
+      cleanup();
+      return -4;
+    }
+    const int widths[6] = {32, 16, 8, 4, 2, 1};
+    std::vector<ClassPlan> plan;
+    int64_t i = 0;
+    for (int c = 0; c < 6 && i < count; ++c) {
+      const int W = widths[c];
+      const int64_t lo_p = (W == 1) ? 0 : 16 * W;  // (32*W/2, 32*W]
+      int64_t j = i;
+      while (j < count && pofkey(hk[j]) > lo_p) ++j;
+      if (W == 1)
+        while (j < count && pofkey(hk[j]) >= 0) ++j;
+      if (j > i) plan.push_back({W, i, j - i});
+      i = j;
+    }
+    const int64_t trivial_begin = i;  // first-level roots with P empty
+    const int64_t trivial_count = count - i;
+    int64_t wcap = 0;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    double frac = cfg->mem_fraction > 0 ? cfg->mem_fraction : 0.5;
+    size_t budget = (size_t)(free_b * frac);
+    // per-worker metrics accumulate across class launches
+    int64_t metric_slots = 0;
+    {
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      metric_slots = cfg->workers > 0 ? cfg->workers : (int64_t)sms * 64;
+    }
+    if (get(&wmet, metric_slots * 4)) {
+      cleanup();
+      return -1;
+    }
+    MCE_CHECK(cudaMemsetAsync(wmet, 0, sizeof(long long) * 4 * metric_slots, s));
+    for (const ClassPlan& cp : plan) {
+      EnumArgs args{};
+      args.n = n;
+      args.ro = g->ro;
+      args.col = g->col;
+      args.split = g->split;
+      args.vhash = vhash;
+      args.roots = sorted_roots + cp.begin;
+      args.num_roots = cp.count;
+      args.roots_mode = cfg->roots;
+      args.xcap = g->max_earlier;
+      args.g_acc = acc;
+      args.g_hist = hist;
+      args.w_metrics = wmet;
+      args.collect = d_collect;
+      args.collect_cap = cfg->collect_cap;
+      args.collect_len = collect_len;
+      args.worker_list_on = cfg->worker_list;
+      args.min_p = cfg->donation_min_p;
+      int req = cfg->workers > 0 ? cfg->workers : 0;
+      if (req <= 0) req = 0;
+      int rc = cfg->induced_full
+                   ? launch_W<true>(cp.W, args, req, &workers_used, s, &launches, budget)
+                   : launch_W<false>(cp.W, args, req, &workers_used, s, &launches, budget);
+      if (rc) {
+        cleanup();
+        return rc;
+      }
+      wcap = std::max<int64_t>(wcap, req > 0 ? req : metric_slots);
+    }
+    max_workers_slots = std::max<int64_t>(workers_used, 1);
+    if (trivial_count > 0) {
+      k_trivial_roots<<<grid_for(trivial_count), 256, 0, s>>>(
+          sorted_roots + trivial_begin, trivial_count, g->ro, g->split, vhash, acc, hist,
+          d_collect, cfg->collect_cap, collect_len);
+      MCE_CHECK(cudaGetLastError());
+      trivial_nodes = trivial_count;  // one visited node each (scheduler.py:300-301)
+    }
+    (void)wcap;
+  }
+  if (cfg->roots == 2 && cfg->include_isolated) {
+    int64_t* all = nullptr;
+    if (get(&all, n)) {
+      cleanup();
+      return -1;
+    }
+    k_isolated<<<grid_for(n), 256, 0, s>>>(n, g->ro, all);
+    k_trivial_roots<<<grid_for(n), 256, 0, s>>>(all, n, g->ro, g->split, vhash, acc, hist,
+                                                 d_collect, cfg->collect_cap, collect_len);
+    MCE_CHECK(cudaGetLastError());
+  }
+  unsigned long long h_acc[8];
+  unsigned long long h_len = 0;
+  MCE_CHECK(cudaMemcpyAsync(h_acc, acc, sizeof(h_acc), cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaMemcpyAsync(out->hist, hist, sizeof(int64_t) * HIST_MAX, cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaMemcpyAsync(&h_len, collect_len, sizeof(h_len), cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaStreamSynchronize(s));
+  if (collect && cfg->collect_cap > 0) {
+    int64_t words = std::min<int64_t>((int64_t)h_len, cfg->collect_cap);
+    if (words > 0)
+      MCE_CHECK(cudaMemcpyAsync(collect, d_collect, sizeof(int64_t) * words,
+                                cudaMemcpyDeviceToHost, s));
+  }
+  if (worker_metrics && wmet && worker_metrics_cap > 0) {
+    int64_t slots = std::min<int64_t>(worker_metrics_cap, max_workers_slots);
+    if (slots > 0)
+      MCE_CHECK(cudaMemcpyAsync(worker_metrics, wmet, sizeof(int64_t) * 4 * slots,
+                                cudaMemcpyDeviceToHost, s));
+  }
+  MCE_CHECK(cudaStreamSynchronize(s));
+  out->cliques = (int64_t)h_acc[0];
+  out->hash = (uint64_t)h_acc[1];
+  out->nodes = (int64_t)h_acc[2] + trivial_nodes;
+  if (worker_metrics && worker_metrics_cap > 0) worker_metrics[0] += trivial_nodes;
+  out->donations = (int64_t)h_acc[3];
+  out->max_size = (int64_t)h_acc[4];
+  out->workers = max_workers_slots;
+  out->launches = launches;
+  out->collect_len = (int64_t)h_len;
+  cleanup();
+  return 0;
+}
+
+}  // extern "C"

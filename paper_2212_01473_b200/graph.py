@@ -1,0 +1,325 @@
+"""Graph ingestion, canonicalisation, statistics and degeneracy ordering.
+
+Same API as the reference ``mce.graph`` (reference graph.py:1-243): a
+canonical undirected simple graph in CSR form with strictly ascending
+adjacency rows.  The difference is where the work happens: canonicalisation
+(``from_edges``), degeneracy ordering and reordering run as CUDA kernels in
+libmce_b200.so and the graph stays resident in HBM; the numpy CSR arrays of
+the reference's dataclass are materialised only when host code reads them.
+
+``degeneracy_order`` takes ``method``:
+
+* ``"parallel"`` (default) -- bucket peeling on the GPU: every vertex whose
+  current degree is at most the peel level leaves in the same round, ranked
+  by id.  A valid degeneracy ordering with exactly the reference's
+  degeneracy ``d`` (so |P| <= d for every first-level root), but not the same
+  permutation.
+* ``"exact"`` -- the reference's own order (minimum current degree, ties to
+  the smallest id; graph.py:189-218), computed by a single-CTA kernel;
+  positions are bit-identical to the reference.
+
+Clique results never depend on the method: counts, size histograms and the
+clique-set hash (over original labels) are identical; only traversal-tree
+sizes differ.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import io
+from dataclasses import dataclass
+from typing import IO, Iterable
+
+import numpy as np
+
+from paper_2212_01473_b200 import _lib
+
+ORDER_METHODS = {"parallel": 0, "exact": 1}
+
+
+class EdgeListParseError(ValueError):
+    """Malformed edge-list input; carries the 1-based line number
+    (reference graph.py:18-24)."""
+
+    def __init__(self, line_no: int, message: str) -> None:
+        super().__init__(f"line {line_no}: {message}")
+        self.line_no = line_no
+
+
+class _DeviceGraph:
+    """Owns one ``mce_graph*`` (device-resident CSR)."""
+
+    __slots__ = ("handle",)
+
+    def __init__(self, handle: ctypes.c_void_p) -> None:
+        self.handle = handle
+
+    def __del__(self) -> None:
+        h, self.handle = self.handle, None
+        if h and _lib._lib is not None:
+            _lib._lib.mce_graph_free(h)
+
+    def info(self) -> dict:
+        vals = [ctypes.c_int64() for _ in range(5)]
+        _lib.check(_lib.lib().mce_graph_info(self.handle, *[ctypes.byref(v) for v in vals]),
+                   "mce_graph_info")
+        n, nnz, maxdeg, later, earlier = (v.value for v in vals)
+        return {"n": n, "nnz": nnz, "max_degree": maxdeg, "max_later": later,
+                "max_earlier": earlier}
+
+
+class Graph:
+    """Undirected simple graph in CSR form (reference graph.py:27-93).
+
+    ``row_offsets`` (n+1) and ``col_indices`` (2m, rows strictly ascending)
+    are numpy views materialised on demand from the device copy; ``labels``
+    (original vertex id of every vertex) is set on reordered graphs.
+    """
+
+    def __init__(self, num_vertices: int, row_offsets: np.ndarray | None = None,
+                 col_indices: np.ndarray | None = None, edge_list: np.ndarray | None = None,
+                 *, _device: _DeviceGraph | None = None, _labels: np.ndarray | None = None):
+        self.num_vertices = int(num_vertices)
+        self._ro = None if row_offsets is None else np.asarray(row_offsets, dtype=np.int64)
+        self._ci = None if col_indices is None else np.asarray(col_indices, dtype=np.int64)
+        self.edge_list = edge_list
+        self._dev = _device
+        self._labels = _labels
+        self._info: dict | None = None
+        if self._dev is None and (self._ro is None or self._ci is None):
+            raise ValueError("Graph needs CSR arrays or a device graph")
+
+    # --- device / host residency ---------------------------------------
+    @property
+    def device(self) -> _DeviceGraph:
+        """The device-resident copy (uploaded from the CSR arrays if needed)."""
+        if self._dev is None:
+            ro = np.ascontiguousarray(self._ro, dtype=np.int64)
+            ci = np.ascontiguousarray(self._ci, dtype=np.int64)
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().mce_graph_from_csr(_lib.ptr(ro), _lib.ptr(ci),
+                                                     self.num_vertices, len(ci), 0, None,
+                                                     ctypes.byref(h)), "mce_graph_from_csr")
+            self._dev = _DeviceGraph(h)
+        return self._dev
+
+    def _materialize(self) -> None:
+        info = self.device_info()
+        ro = np.empty(self.num_vertices + 1, dtype=np.int64)
+        ci = np.empty(info["nnz"], dtype=np.int64)
+        _lib.check(_lib.lib().mce_graph_copy_csr(self._dev.handle, _lib.ptr(ro), _lib.ptr(ci),
+                                                 None, None), "mce_graph_copy_csr")
+        self._ro, self._ci = ro, ci
+
+    def device_info(self) -> dict:
+        if self._info is None:
+            self._info = self.device.info()
+        return self._info
+
+    @property
+    def row_offsets(self) -> np.ndarray:
+        if self._ro is None:
+            self._materialize()
+        return self._ro
+
+    @property
+    def col_indices(self) -> np.ndarray:
+        if self._ci is None:
+            self._materialize()
+        return self._ci
+
+    @property
+    def labels(self) -> np.ndarray | None:
+        """Original label of every vertex (reordered graphs), else None."""
+        return self._labels
+
+    # --- reference accessors ---------------------------------------------
+    def neighbors(self, v: int) -> np.ndarray:
+        ro = self.row_offsets
+        return self.col_indices[ro[v]:ro[v + 1]]
+
+    def degree(self, v: int) -> int:
+        ro = self.row_offsets
+        return int(ro[v + 1] - ro[v])
+
+    @property
+    def num_edges(self) -> int:
+        if self._ci is not None:
+            return len(self._ci) // 2
+        return self.device_info()["nnz"] // 2
+
+    def has_edge(self, u: int, v: int) -> bool:
+        adj = self.neighbors(u)
+        i = int(np.searchsorted(adj, v))
+        return i < len(adj) and adj[i] == v
+
+    def edges(self) -> np.ndarray:
+        """All undirected edges as an (m, 2) array with u < v, cached."""
+        if self.edge_list is None:
+            ro, ci = self.row_offsets, self.col_indices
+            src = np.repeat(np.arange(self.num_vertices, dtype=np.int64), np.diff(ro))
+            keep = src < ci
+            self.edge_list = np.column_stack((src[keep], ci[keep]))
+        return self.edge_list
+
+    def validate(self) -> None:
+        """Check the CSR invariants (reference graph.py:61-76); raises ValueError."""
+        ro, ci = self.row_offsets, self.col_indices
+        n = self.num_vertices
+        if len(ro) != n + 1 or ro[0] != 0 or ro[-1] != len(ci):
+            raise ValueError("row_offsets inconsistent with col_indices")
+        if np.any(np.diff(ro) < 0):
+            raise ValueError("row_offsets not non-decreasing")
+        src = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
+        if len(ci):
+            if np.any(ci == src) or np.any(ci < 0) or np.any(ci >= n):
+                raise ValueError("self-loop or out-of-range neighbour")
+            same_row = src[1:] == src[:-1]
+            if np.any(same_row & (ci[1:] <= ci[:-1])):
+                raise ValueError("adjacency not strictly ascending")
+        fwd = src * np.int64(max(n, 1)) + ci
+        rev = ci * np.int64(max(n, 1)) + src
+        if not np.array_equal(np.sort(fwd), np.sort(rev)):
+            raise ValueError("adjacency not symmetric")
+
+    def __repr__(self) -> str:
+        return f"Graph(num_vertices={self.num_vertices}, num_edges={self.num_edges})"
+
+
+@dataclass(frozen=True)
+class GraphStats:
+    """Headline numbers: size, max degree, degeneracy (reference graph.py:79-87)."""
+
+    n: int
+    m: int
+    max_degree: int
+    degeneracy: int
+
+
+@dataclass(frozen=True)
+class DegeneracyOrder:
+    """Permutation original id -> rank plus the degeneracy it realises."""
+
+    position: np.ndarray
+    degeneracy: int
+
+
+def _from_device(n: int, h: ctypes.c_void_p, labels: np.ndarray | None = None) -> Graph:
+    return Graph(n, _device=_DeviceGraph(h), _labels=labels)
+
+
+def from_edges(edges: Iterable[tuple[int, int]] | np.ndarray, num_vertices: int) -> Graph:
+    """Canonical graph from compacted vertex pairs, built on the GPU
+    (reference graph.py:96-120): self-loops dropped, duplicates merged,
+    both directions stored, rows ascending."""
+    arr = np.ascontiguousarray(
+        np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges,
+                   dtype=np.int64).reshape(-1, 2))
+    if arr.size and (arr.min() < 0 or arr.max() >= num_vertices):
+        raise ValueError("vertex id outside [0, num_vertices)")
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().mce_graph_from_edges(_lib.ptr(arr), len(arr), int(num_vertices), 0,
+                                               None, ctypes.byref(h)), "mce_graph_from_edges")
+    return _from_device(num_vertices, h)
+
+
+def from_device_edges(edges_dev, num_edges: int, num_vertices: int, stream=None) -> Graph:
+    """Canonical graph from an edge buffer already in device memory
+    (int64 pairs; e.g. a torch CUDA tensor or mce_gen_rmat output)."""
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().mce_graph_from_edges(_lib.ptr(edges_dev), int(num_edges),
+                                               int(num_vertices), 1, stream, ctypes.byref(h)),
+               "mce_graph_from_edges")
+    return _from_device(num_vertices, h)
+
+
+def parse_edge_list(source: str | IO[str], base: int = 0, symmetrize: bool = True) -> Graph:
+    """Parse whitespace-separated edge-list text into a canonical graph
+    (reference graph.py:123-175): '#'/'%' comments, MatrixMarket header
+    switches to 1-based ids and skips the size line, ids are compacted to
+    [0, n), duplicates merge, self-loops drop, output always symmetric."""
+    del symmetrize
+    stream = io.StringIO(source) if isinstance(source, str) else source
+    us: list[int] = []
+    vs: list[int] = []
+    matrix_market = False
+    size_pending = False
+    for line_no, line in enumerate(stream, start=1):
+        text = line.strip()
+        if not text:
+            continue
+        if text.startswith("%%MatrixMarket"):
+            matrix_market, size_pending, base = True, True, 1
+            continue
+        if text[0] in "#%":
+            continue
+        if size_pending:
+            size_pending = False
+            continue
+        tok = text.split()
+        if len(tok) < 2 or (len(tok) > 2 and not matrix_market):
+            raise EdgeListParseError(line_no, f"expected two integer tokens, got {text!r}")
+        try:
+            u, v = int(tok[0]) - base, int(tok[1]) - base
+        except ValueError as exc:
+            raise EdgeListParseError(line_no, f"non-integer token in {text!r}") from exc
+        if u < 0 or v < 0:
+            raise EdgeListParseError(line_no, f"vertex id below base in {text!r}")
+        us.append(u)
+        vs.append(v)
+    if not us:
+        return from_edges(np.empty((0, 2), dtype=np.int64), 0)
+    raw = np.column_stack((np.asarray(us, dtype=np.int64), np.asarray(vs, dtype=np.int64)))
+    ids, compact = np.unique(raw, return_inverse=True)
+    return from_edges(compact.reshape(-1, 2).astype(np.int64), len(ids))
+
+
+def degeneracy_order(g: Graph, method: str = "parallel") -> DegeneracyOrder:
+    """Degeneracy ordering on the GPU (reference graph.py:189-218); see the
+    module docstring for ``method``."""
+    if method not in ORDER_METHODS:
+        raise ValueError(f"unknown ordering method {method!r}")
+    n = g.num_vertices
+    pos = np.empty(n, dtype=np.int64)
+    d = ctypes.c_int64(0)
+    if n:
+        _lib.check(_lib.lib().mce_degeneracy_order(g.device.handle, ORDER_METHODS[method],
+                                                   _lib.ptr(pos), 0, ctypes.byref(d), None),
+                   "mce_degeneracy_order")
+    return DegeneracyOrder(pos, int(d.value))
+
+
+def reorder(g: Graph, order: DegeneracyOrder) -> Graph:
+    """Relabel vertices by rank on the GPU (reference graph.py:221-232)."""
+    pos = np.ascontiguousarray(order.position, dtype=np.int64)
+    if len(pos) != g.num_vertices:
+        raise ValueError("permutation length does not match vertex count")
+    n = g.num_vertices
+    if n == 0:
+        return from_edges(np.empty((0, 2), dtype=np.int64), 0)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().mce_reorder(g.device.handle, _lib.ptr(pos), 0, None, ctypes.byref(h)),
+               "mce_reorder")
+    base = g.labels if g.labels is not None else np.arange(n, dtype=np.int64)
+    labels = np.empty(n, dtype=np.int64)
+    labels[pos] = base
+    return _from_device(n, h, labels)
+
+
+def stats(g: Graph, order: DegeneracyOrder) -> GraphStats:
+    """Vertex/edge counts, maximum degree and the ordering's degeneracy."""
+    if g.num_vertices == 0:
+        return GraphStats(0, 0, 0, order.degeneracy)
+    if g._ro is not None:
+        max_degree = int(np.diff(g._ro).max())
+    else:
+        max_degree = g.device_info()["max_degree"]
+    return GraphStats(n=g.num_vertices, m=g.num_edges, max_degree=max_degree,
+                      degeneracy=order.degeneracy)
+
+
+def preprocess(g: Graph, method: str = "parallel") -> tuple[Graph, DegeneracyOrder, GraphStats]:
+    """Order, relabel and summarise in one step (reference graph.py:238-243)."""
+    order = degeneracy_order(g, method=method)
+    g2 = reorder(g, order)
+    return g2, order, stats(g2, order)

@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Bit-exact on every integer output:
+degeneracy / positions, clique count, search-tree node total, size
+histogram and clique-set hash."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import K4_TRIANGLE_CLIQUES, K4_TRIANGLE_EDGES, golden_cases
+from oracle import oracle
+from paper_2212_01473_b200 import (
+    CliqueSink,
+    RunConfig,
+    degeneracy_order,
+    from_edges,
+    preprocess,
+    reorder,
+    run,
+    stats,
+)
+
+pytestmark = pytest.mark.gpu
+
+CASES = golden_cases()
+MODES = ["l1-ipx", "l1-ip", "l2-ipx", "l2-ip"]
+
+
+def _graph(case):
+    edges = np.asarray(case["edges"], dtype=np.int64).reshape(-1, 2)
+    return from_edges(edges, case["n"]), edges
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_csr_and_orderings_match_reference(case):
+    g, edges = _graph(case)
+    ro, ci = oracle.from_edges(edges, case["n"])
+    assert np.array_equal(g.row_offsets, ro)
+    assert np.array_equal(g.col_indices, ci)
+    exact = degeneracy_order(g, method="exact")
+    assert exact.degeneracy == case["degeneracy"]
+    assert exact.position.tolist() == case["position"]
+    par = degeneracy_order(g, method="parallel")
+    assert par.degeneracy == case["degeneracy"]
+    assert sorted(par.position.tolist()) == list(range(case["n"]))
+    g2 = reorder(g, par)
+    n = case["n"]
+    if n:
+        later = [int(np.sum(g2.neighbors(v) > v)) for v in range(n)]
+        assert max(later) == case["degeneracy"]  # a degeneracy ordering, tight
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_exact_order_runs_match_reference_bit_for_bit(case):
+    """Reference ordering -> identical traversal tree: count, nodes, hist, hash."""
+    g, _ = _graph(case)
+    order = degeneracy_order(g, method="exact")
+    g2 = reorder(g, order)
+    st = stats(g2, order)
+    assert st.max_degree == case["max_degree"] and st.m == case["m"]
+    for mode in MODES:
+        exp = case["runs"][mode]
+        roots, induced = mode.split("-")
+        res = run(g2, st, RunConfig(workers=8, roots=roots, induced=induced))
+        assert res.clique_count == exp["count"], mode
+        assert res.nodes_total == exp["nodes"], mode
+        if "hash" in exp:
+            assert res.clique_hash_hex == exp["hash"], mode
+            assert {str(k): v for k, v in res.size_histogram.items()} == exp["hist"], mode
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["n"] >= 64],
+                         ids=[c["name"] for c in CASES if c["n"] >= 64])
+def test_parallel_order_results_and_tree_match_oracle(case):
+    """Parallel ordering: same cliques (count/hist/hash over original labels);
+    the node total equals the oracle's on the GPU-reordered graph."""
+    g, _ = _graph(case)
+    g2, order, st = preprocess(g)
+    ro2, ci2 = g2.row_offsets, g2.col_indices
+    for mode in MODES:
+        exp = case["runs"][mode]
+        roots, induced = mode.split("-")
+        res = run(g2, st, RunConfig(roots=roots, induced=induced))
+        assert res.clique_count == exp["count"], mode
+        assert res.clique_hash_hex == exp["hash"], mode
+        assert {str(k): v for k, v in res.size_histogram.items()} == exp["hist"], mode
+        orc = oracle.enumerate_cliques(ro2, ci2, roots=roots, induced=induced,
+                                       degeneracy=st.degeneracy, labels=g2.labels)
+        assert res.nodes_total == orc["nodes"], mode
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "brute_force" in c],
+                         ids=[c["name"] for c in CASES if "brute_force" in c])
+def test_collected_cliques_match_brute_force(case):
+    g, _ = _graph(case)
+    g2, order, st = preprocess(g)
+    inverse = np.argsort(order.position)
+    expected = {tuple(c) for c in case["brute_force"]}
+    for mode in MODES:
+        roots, induced = mode.split("-")
+        sink = CliqueSink.collecting()
+        res = run(g2, st, RunConfig(workers=4, roots=roots, induced=induced), sink=sink)
+        got = {tuple(sorted(int(inverse[v]) for v in c)) for c in sink.collected}
+        assert got == expected, mode
+        assert res.clique_count == len(expected) == sink.total
+
+
+def test_running_example():
+    g = from_edges(K4_TRIANGLE_EDGES, 6)
+    g2, order, st = preprocess(g)
+    inverse = np.argsort(order.position)
+    for roots in ("l1", "l2"):
+        for induced in ("ip", "ipx"):
+            for wl in (True, False):
+                sink = CliqueSink(collect_limit=10)
+                res = run(g2, st, RunConfig(workers=2, roots=roots, induced=induced,
+                                            worker_list=wl), sink=sink)
+                assert res.clique_count == 2
+                got = {tuple(sorted(int(inverse[v]) for v in c)) for c in sink.collected}
+                assert got == K4_TRIANGLE_CLIQUES
+
+
+def test_work_conservation_across_workers_and_donation():
+    """Reference acceptance criterion 4: the node total is invariant across
+    worker counts and worker-list on/off (the traversal tree is identical)."""
+    for case in CASES:
+        if case["name"] not in ("gnp_200_0.5_s3", "skew_2000_40", "gnp_300_0.08_s42"):
+            continue
+        g, _ = _graph(case)
+        g2, _, st = preprocess(g, method="exact")
+        for mode in ("l1-ipx", "l1-ip"):
+            roots, induced = mode.split("-")
+            totals, counts = set(), set()
+            for workers in (1, 2, 4, 8, 16, 0):
+                for wl in (True, False):
+                    res = run(g2, st, RunConfig(workers=workers, roots=roots, induced=induced,
+                                                worker_list=wl, donation_min_p=4))
+                    totals.add(sum(w.nodes_visited for w in res.worker_metrics))
+                    counts.add(res.clique_count)
+                    made = sum(w.donations_made for w in res.worker_metrics)
+                    recv = sum(w.donations_received for w in res.worker_metrics)
+                    assert made == recv == res.donation_count
+                    if not wl:
+                        assert made == 0
+            assert totals == {case["runs"][mode]["nodes"]}, (case["name"], mode, totals)
+            assert counts == {case["runs"][mode]["count"]}
+
+
+def test_donations_happen_and_preserve_results():
+    """A skewed instance with few workers must actually donate, and the
+    donated run must reproduce count, hash and node total."""
+    case = next(c for c in CASES if c["name"] == "gnp_200_0.5_s3")
+    g, _ = _graph(case)
+    g2, _, st = preprocess(g, method="exact")
+    base = run(g2, st, RunConfig(workers=1, induced="ipx", worker_list=False))
+    res = run(g2, st, RunConfig(workers=64, induced="ipx", donation_min_p=2))
+    assert res.clique_count == base.clique_count == case["runs"]["l1-ipx"]["count"]
+    assert res.clique_hash == base.clique_hash
+    assert res.nodes_total == base.nodes_total == case["runs"]["l1-ipx"]["nodes"]
+    assert res.donation_count > 0
+
+
+def test_edge_cases():
+    for edges, n in (([], 0), ([], 4), ([(0, 1)], 2), ([(0, 1), (1, 2), (0, 2)], 5)):
+        g = from_edges(np.asarray(edges, dtype=np.int64).reshape(-1, 2), n)
+        g2, _, st = preprocess(g)
+        ro, ci = oracle.from_edges(np.asarray(edges, dtype=np.int64).reshape(-1, 2), n)
+        pos, d = oracle.degeneracy_order(ro, ci)
+        for roots in ("l1", "l2"):
+            exp = oracle.reference_pipeline(np.asarray(edges, dtype=np.int64).reshape(-1, 2),
+                                            n, roots=roots, induced="ipx")
+            res = run(g2, st, RunConfig(workers=2, roots=roots, induced="ipx"))
+            assert res.clique_count == exp["count"]
+            if n:
+                assert res.clique_hash_hex == exp["hash"]
+
+
+def test_l2_roots_count_isolated_vertices():
+    g = from_edges([(0, 1), (1, 2), (0, 2)], 5)
+    g2, _, st = preprocess(g)
+    res = run(g2, st, RunConfig(workers=2, roots="l2", induced="ipx"))
+    assert res.clique_count == 3

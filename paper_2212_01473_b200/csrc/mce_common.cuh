@@ -45,4 +45,8 @@ struct mce_graph {
 
 int mce_graph_build_split(mce_graph* g, cudaStream_t s);
 
+// Keep freed stream-ordered allocations in the device pool (repeated runs
+// reuse HBM instead of returning it to the driver at every synchronisation).
+void mce_prepare_device();
+
 static inline int mce_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

@@ -40,14 +40,16 @@ constexpr int HIST_SMEM = 128;
 constexpr int HIST_MAX = MCE_HIST_MAX;
 constexpr unsigned FULLMASK = 0xffffffffu;
 
+// Lock-free worker list (paper §3.3, reference scheduler.py:99-165).  A parked
+// worker sets its bit in `idle_bits`; a donor claims a receiver by clearing
+// that bit with atomicAnd (each parked id is claimed at most once).  `state`
+// packs the idle count (high 32 bits) and the donations in flight (low 32)
+// so the termination test "every worker parked and nothing in flight" is a
+// single atomic read-modify-write.
 struct WorkerListDev {
-  int lock;
-  int head;
-  int count;
-  int idle;
-  int in_flight;
+  unsigned long long state;
   int terminated;
-  int pad[2];
+  int pad;
 };
 
 struct Mailbox {
@@ -93,7 +95,7 @@ struct EnumArgs {
   unsigned long long* collect_len;
   // worker list
   WorkerListDev* wl;
-  int* wl_ring;
+  unsigned* idle_bits;  // ceil(num_workers / 32) words
   int* wl_wake;
   Mailbox* mbox;
   int worker_list_on;
@@ -119,17 +121,7 @@ __device__ __forceinline__ bool contains_range(const int32_t* __restrict__ col, 
   return lo < end && col[lo] == key;
 }
 
-__device__ __forceinline__ void spin_lock(int* l) {
-  while (atomicCAS(l, 0, 1) != 0) __nanosleep(32);
-  __threadfence();
-}
-
-__device__ __forceinline__ void spin_unlock(int* l) {
-  __threadfence();
-  atomicExch(l, 0);
-}
-
-template <int W, bool FULL, bool ROWS_SMEM>
+template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM>
 struct Worker {
   static constexpr int CAP = 32 * W;
   static constexpr int CAPP = CAP + 1;
@@ -167,7 +159,7 @@ struct Worker {
       rowsT = a.rows_g + (size_t)wid * W * CAPP;
       plist = a.plist_g + (size_t)wid * CAP;
     }
-    xrowsT = FULL ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
+    xrowsT = XROWS ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
     xlist_buf = a.xlist ? a.xlist + (size_t)wid * a.xcap : nullptr;
     xx = a.xx + (size_t)wid * a.xcap;
     xtmp = a.xtmp + (size_t)wid * a.xcap;
@@ -251,7 +243,7 @@ struct Worker {
         }
       }
     }
-    if (FULL) {
+    if (XROWS) {
       // X rows (induced.py:90-98): X member x is earlier than every P vertex,
       // so its P-neighbours are N+(x) & P.  Lane t owns column t.
       for (int t = lane; t < nx; t += 32) {
@@ -270,7 +262,7 @@ struct Worker {
 
   // ---------------------------------------------------------------- pieces
   __device__ __forceinline__ bool xx_adjacent(int32_t t, int v, int32_t gv) const {
-    if (FULL) return (xrowsT[(size_t)(v >> 5) * a.xcap + t] >> (v & 31)) & 1u;
+    if (XROWS) return (xrowsT[(size_t)(v >> 5) * a.xcap + t] >> (v & 31)) & 1u;
     const int32_t x = root_x[t];
     return contains_range(a.col, a.split[x], a.ro[x + 1], gv);
   }
@@ -332,7 +324,7 @@ struct Worker {
     const int pc = __reduce_min_sync(FULLMASK, best == m ? bestc : 0x7fffffff);
     uint32_t prow;
     bool use_local = true;
-    if (FULL && live > 0) {
+    if (PIVOT_XX && live > 0) {
       int xb = -1, xpos = 0x7fffffff;
       for (int base = 0; base < live; base += 32) {
         const int i = base + lane;
@@ -394,17 +386,29 @@ struct Worker {
   __device__ bool try_donate(uint32_t childP, uint32_t childXP, int v, int32_t gv, int live,
                              int rlen) {
     int rid = -1;
-    if (lane == 0) {
-      WorkerListDev* wl = a.wl;
-      if (*(volatile int*)&wl->count > 0) {
-        spin_lock(&wl->lock);
-        if (wl->count > 0 && !wl->terminated) {
-          rid = a.wl_ring[wl->head];
-          wl->head = (wl->head + 1) % a.num_workers;
-          wl->count--;
-          wl->in_flight++;
+    const unsigned long long st = *(volatile unsigned long long*)&a.wl->state;
+    if ((st >> 32) == 0) return false;  // nobody parked
+    const int nwords = (a.num_workers + 31) >> 5;
+    const int start = (wid * 7) % nwords;
+    for (int base = 0; base < nwords && rid < 0; base += 32) {
+      const int wi = (start + base + lane) % nwords;
+      const unsigned bits = (base + lane < nwords) ? *(volatile unsigned*)&a.idle_bits[wi] : 0u;
+      unsigned m = __ballot_sync(FULLMASK, bits != 0);
+      while (m && rid < 0) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const unsigned wbits = __shfl_sync(FULLMASK, bits, src);
+        const int word = __shfl_sync(FULLMASK, wi, src);
+        const int b = __ffs(wbits) - 1;
+        int claimed = -1;
+        if (lane == 0) {
+          const unsigned old = atomicAnd(&a.idle_bits[word], ~(1u << b));
+          if (old & (1u << b)) {
+            claimed = word * 32 + b;
+            atomicAdd(&a.wl->state, 1ull);  // one more donation in flight
+          }
         }
-        spin_unlock(&wl->lock);
+        rid = __shfl_sync(FULLMASK, claimed, 0);
       }
     }
     rid = __shfl_sync(FULLMASK, rid, 0);
@@ -444,35 +448,28 @@ struct Worker {
     int got = 0;
     if (lane == 0) {
       WorkerListDev* wl = a.wl;
-      bool done = false;
-      spin_lock(&wl->lock);
-      if (wl->terminated) {
-        done = true;
-      } else if (wl->idle + 1 == a.num_workers && wl->in_flight == 0) {
-        wl->terminated = 1;
-        for (int i = 0; i < a.num_workers; ++i) atomicExch(&a.wl_wake[i], 1);
-        done = true;
+      const unsigned long long now = atomicAdd(&wl->state, 1ull << 32) + (1ull << 32);
+      if ((now >> 32) == (unsigned long long)a.num_workers && (now & 0xffffffffull) == 0) {
+        atomicExch(&wl->terminated, 1);  // last one in with nothing in flight
       } else {
-        wl->idle++;
-        a.wl_ring[(wl->head + wl->count) % a.num_workers] = wid;
-        wl->count++;
-      }
-      spin_unlock(&wl->lock);
-      if (!done) {
-        unsigned ns = 64;
-        while (*(volatile int*)&a.wl_wake[wid] == 0) {
+        atomicOr(&a.idle_bits[wid >> 5], 1u << (wid & 31));
+        unsigned ns = 32;
+        for (;;) {
+          if (*(volatile int*)&a.wl_wake[wid]) {
+            got = 1;
+            break;
+          }
+          if (*(volatile int*)&wl->terminated) break;
           __nanosleep(ns);
-          ns = ns < 8192 ? ns * 2 : ns;
+          ns = ns < 4096 ? ns * 2 : ns;
         }
-        __threadfence();
-        spin_lock(&wl->lock);
-        a.wl_wake[wid] = 0;
-        Mailbox* mb = a.mbox + wid;
-        got = mb->has_task;
-        mb->has_task = 0;
-        wl->idle--;
-        if (got) wl->in_flight--;
-        spin_unlock(&wl->lock);
+        if (got) {
+          __threadfence();
+          a.wl_wake[wid] = 0;
+          a.mbox[wid].has_task = 0;
+          // leave the idle set and retire the in-flight donation together
+          atomicAdd(&wl->state, ~0ull - (1ull << 32));  // -= (1<<32) + 1
+        }
       }
     }
     got = __shfl_sync(FULLMASK, got, 0);
@@ -607,7 +604,7 @@ struct Worker {
   }
 };
 
-template <int W, bool FULL, bool ROWS_SMEM, int WARPS>
+template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
@@ -622,7 +619,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
   __syncthreads();
   const int wid = blockIdx.x * WARPS + warp;
   if (wid < a.num_workers) {
-    Worker<W, FULL, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
+    Worker<W, PIVOT_XX, XROWS, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
                                   s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + warp * 32,
                                   s_hist);
     for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-260)
@@ -659,18 +656,35 @@ __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
 
 // ------------------------------------------------------------ root prep
 
-// l1 roots: |P| = |N+(v)|; l2 roots: edges (u < v) with bound |N+(v)|
+// Root keys: class (bitset width) in the top byte, then heaviest-first by an
+// estimated subtree cost.  l1 roots: |P| = |N+(v)|, |X| = |N-(v)|; l2 roots
+// (edges u < v): bounded by |N+(v)| and |N-(v)|.
+__device__ __forceinline__ int width_rank(int64_t p) {
+  if (p > 512) return 0;   // W = 32
+  if (p > 256) return 1;   // 16
+  if (p > 128) return 2;   // 8
+  if (p > 64) return 3;    // 4
+  if (p > 32) return 4;    // 2
+  return 5;                // 1
+}
+
 __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
                             const int32_t* __restrict__ col, const int64_t* __restrict__ eoff,
                             int64_t n, int roots_mode, int64_t begin, int64_t stride,
-                            int64_t count, uint32_t* __restrict__ keys,
-                            int64_t* __restrict__ roots) {
+                            int64_t count, uint64_t* __restrict__ keys,
+                            int64_t* __restrict__ roots, unsigned long long* __restrict__ classes,
+                            unsigned long long* __restrict__ max_p) {
+  __shared__ unsigned long long s_cls[8];
+  if (threadIdx.x < 8) s_cls[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long local_max = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = begin + i * stride;
-    int64_t p;
+    int64_t p, x;
     if (roots_mode == 1) {
       p = ro[r + 1] - split[r];
+      x = split[r] - ro[r];
       roots[i] = r;
     } else {
       int64_t lo = 0, hi = n;  // largest u with eoff[u] <= r
@@ -681,12 +695,20 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
       const int64_t u = lo;
       const int64_t v = col[split[u] + (r - eoff[u])];
       p = ro[v + 1] - split[v];
+      x = split[v] - ro[v];
       roots[i] = (u << 32) | v;
     }
-    // ascending key = descending |P| (heavy subtrees first); zero-P first-level
-    // roots get the largest key and are counted without a worker
-    keys[i] = (roots_mode == 1 && p == 0) ? 0xffffffffu : (uint32_t)(0x7fffffff - p);
+    const int rank = (roots_mode == 1 && p == 0) ? 6 : width_rank(p);
+    uint64_t cost = (uint64_t)(p + 1) * (uint64_t)(p + 1) + (uint64_t)(p + 1) * (uint64_t)x / 8;
+    const uint64_t lim = (1ull << 56) - 1;
+    if (cost > lim) cost = lim;
+    keys[i] = ((uint64_t)rank << 56) | (lim - cost);
+    atomicAdd(&s_cls[rank], 1ull);
+    if ((unsigned long long)p > local_max) local_max = p;
   }
+  __syncthreads();
+  if (threadIdx.x < 7 && s_cls[threadIdx.x]) atomicAdd(&classes[threadIdx.x], s_cls[threadIdx.x]);
+  if (local_max) atomicMax(max_p, local_max);
 }
 
 __global__ void k_later_count(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
@@ -766,12 +788,12 @@ struct ClassPlan {
   int64_t begin, count;  // slice of the sorted root list
 };
 
-template <int W, bool FULL, bool ROWS_SMEM, int WARPS>
+template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
 int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cudaStream_t s,
                  int64_t* launches, size_t mem_budget) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
-  auto kern = k_enumerate<W, FULL, ROWS_SMEM, WARPS>;
+  auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
   size_t smem = HIST_SMEM * sizeof(unsigned long long) + WARPS * 32 * sizeof(uint32_t) +
                 (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
   MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -791,7 +813,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
                       (sizeof(int32_t) + sizeof(uint64_t)) * (levels + 2) +
                       sizeof(int32_t) * 2 * xcap + sizeof(Mailbox) + sizeof(int) * 2 +
                       sizeof(long long) * 4 +
-                      (FULL ? sizeof(uint32_t) * (size_t)W * xcap : 0) +
+                      (XROWS ? sizeof(uint32_t) * (size_t)W * xcap : 0) +
                       (args.roots_mode == 2 ? sizeof(int32_t) * xcap : 0) +
                       (ROWS_SMEM ? 0 : sizeof(uint32_t) * (size_t)(W * CAPP + CAP));
   int64_t by_mem = std::max<int64_t>(1, (int64_t)(mem_budget / per_worker));
@@ -813,7 +835,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   if (get(&args.stack, (size_t)workers * levels * 3 * W) || get(&args.lpx, (size_t)workers * levels) ||
       get(&args.rpath, (size_t)workers * (levels + 2)) || get(&args.hsum, (size_t)workers * (levels + 2)) ||
       get(&args.xx, (size_t)workers * xcap) || get(&args.xtmp, (size_t)workers * xcap) ||
-      get(&args.mbox, (size_t)workers) || get(&args.wl_ring, (size_t)workers) ||
+      get(&args.mbox, (size_t)workers) || get(&args.idle_bits, (size_t)(workers + 31) / 32) ||
       get(&args.wl_wake, (size_t)workers) || get(&args.wl, 1) ||
       get(&args.root_counter, 1))
     return -1;
@@ -821,13 +843,14 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   args.xlist = nullptr;
   args.rows_g = nullptr;
   args.plist_g = nullptr;
-  if (FULL && get(&args.xrows, (size_t)workers * W * xcap)) return -1;
+  if (XROWS && get(&args.xrows, (size_t)workers * W * xcap)) return -1;
   if (args.roots_mode == 2 && get(&args.xlist, (size_t)workers * xcap)) return -1;
   if (!ROWS_SMEM && (get(&args.rows_g, (size_t)workers * W * CAPP) ||
                      get(&args.plist_g, (size_t)workers * CAP)))
     return -1;
   MCE_CHECK(cudaMemsetAsync(args.wl, 0, sizeof(WorkerListDev), s));
   MCE_CHECK(cudaMemsetAsync(args.wl_wake, 0, sizeof(int) * workers, s));
+  MCE_CHECK(cudaMemsetAsync(args.idle_bits, 0, sizeof(unsigned) * ((workers + 31) / 32), s));
   MCE_CHECK(cudaMemsetAsync(args.mbox, 0, sizeof(Mailbox) * workers, s));
   MCE_CHECK(cudaMemsetAsync(args.root_counter, 0, sizeof(unsigned long long), s));
   const int grid = (int)((workers + WARPS - 1) / WARPS);
@@ -838,19 +861,33 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   return 0;
 }
 
-template <bool FULL>
+template <bool PIVOT_XX, bool XROWS>
 int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, int64_t* launches,
              size_t budget) {
   switch (W) {
-    case 1: return launch_class<1, FULL, true, 8>(args, workers, used, s, launches, budget);
-    case 2: return launch_class<2, FULL, true, 8>(args, workers, used, s, launches, budget);
-    case 4: return launch_class<4, FULL, true, 8>(args, workers, used, s, launches, budget);
-    case 8: return launch_class<8, FULL, true, 4>(args, workers, used, s, launches, budget);
-    case 16: return launch_class<16, FULL, true, 2>(args, workers, used, s, launches, budget);
-    case 32: return launch_class<32, FULL, false, 4>(args, workers, used, s, launches, budget);
+    case 1: return launch_class<1, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget);
+    case 2: return launch_class<2, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget);
+    case 4: return launch_class<4, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget);
+    case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget);
+    case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget);
+    case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget);
   }
   mce_set_error("unsupported bitset width %d", W);
   return -3;
+}
+
+// Partial mode ("ip") keeps the reference's pivot rule (P | X_P only) but, when
+// HBM allows, still materialises the X rows so X_X adjacency is one bit test
+// instead of a binary search of the CSR -- same traversal tree, fewer
+// dependent loads.  Full mode ("ipx") always has them.
+int launch_mode(bool full, int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s,
+                int64_t* launches, size_t budget, int64_t resident_guess) {
+  if (full) return launch_W<true, true>(W, args, workers, used, s, launches, budget);
+  const size_t xrows_bytes = sizeof(uint32_t) * (size_t)W * (size_t)std::max<int64_t>(args.xcap, 1) *
+                             (size_t)std::max<int64_t>(resident_guess, 1);
+  if (xrows_bytes <= budget / 2)
+    return launch_W<false, true>(W, args, workers, used, s, launches, budget);
+  return launch_W<false, false>(W, args, workers, used, s, launches, budget);
 }
 
 }  // namespace
@@ -860,6 +897,7 @@ extern "C" {
 int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collect,
                   int64_t* worker_metrics, int64_t worker_metrics_cap, mce_run_result* out,
                   void* stream) {
+  mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   memset(out, 0, sizeof(*out));
   if (cfg->roots != 1 && cfg->roots != 2) {
@@ -922,51 +960,43 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t trivial_nodes = 0;
   int64_t workers_used = 0;
   if (count > 0) {
-    uint32_t *keys = nullptr, *keys2 = nullptr;
+    uint64_t *keys = nullptr, *keys2 = nullptr;
     int64_t *roots = nullptr, *roots2 = nullptr;
-    if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count)) {
+    unsigned long long* cls = nullptr;
+    if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count) ||
+        get(&cls, 8)) {
       cleanup();
       return -1;
     }
+    MCE_CHECK(cudaMemsetAsync(cls, 0, 8 * sizeof(unsigned long long), s));
     k_root_keys<<<grid_for(count), 256, 0, s>>>(g->ro, g->split, g->col, eoff, n, cfg->roots,
-                                                 begin, stride, count, keys, roots);
+                                                 begin, stride, count, keys, roots, cls, cls + 7);
     MCE_CHECK(cudaGetLastError());
-    cub::DoubleBuffer<uint32_t> dk(keys, keys2);
+    cub::DoubleBuffer<uint64_t> dk(keys, keys2);
     cub::DoubleBuffer<int64_t> dv(roots, roots2);
     size_t tb = 0;
-    MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, count, 0, 32, s));
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, count, 0, 64, s));
     void* tmp = nullptr;
     MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
-    MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 32, s));
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 64, s));
     cudaFreeAsync(tmp, s);
-    std::vector<uint32_t> hk(count);
-    MCE_CHECK(cudaMemcpyAsync(hk.data(), dk.Current(), sizeof(uint32_t) * count,
-                              cudaMemcpyDeviceToHost, s));
+    unsigned long long hc[8];
+    MCE_CHECK(cudaMemcpyAsync(hc, cls, sizeof(hc), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
     const int64_t* sorted_roots = dv.Current();
-    // class slices: keys ascending == |P| descending
-    auto pofkey = [](uint32_t k) -> int64_t {
-      return k == 0xffffffffu ? -1 : (int64_t)0x7fffffff - (int64_t)k;
-    };
-    const int64_t cap_limit = cfg->capacity_bits > 0 ? cfg->capacity_bits : 1024;
-    if (pofkey(hk[0]) > std::min<int64_t>(cap_limit, 1024)) {
-      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld",
-                    (long long)pofkey(hk[0]), (long long)std::min<int64_t>(cap_limit, 1024));
+    const int64_t cap_limit = std::min<int64_t>(cfg->capacity_bits > 0 ? cfg->capacity_bits : 1024, 1024);
+    if ((int64_t)hc[7] > cap_limit) {
+      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld", (long long)hc[7],
+                    (long long)cap_limit);
       cleanup();
       return -4;
     }
     const int widths[6] = {32, 16, 8, 4, 2, 1};
     std::vector<ClassPlan> plan;
     int64_t i = 0;
-    for (int c = 0; c < 6 && i < count; ++c) {
-      const int W = widths[c];
-      const int64_t lo_p = (W == 1) ? 0 : 16 * W;  // (32*W/2, 32*W]
-      int64_t j = i;
-      while (j < count && pofkey(hk[j]) > lo_p) ++j;
-      if (W == 1)
-        while (j < count && pofkey(hk[j]) >= 0) ++j;
-      if (j > i) plan.push_back({W, i, j - i});
-      i = j;
+    for (int c = 0; c < 6; ++c) {
+      if (hc[c]) plan.push_back({widths[c], i, (int64_t)hc[c]});
+      i += (int64_t)hc[c];
     }
     const int64_t trivial_begin = i;  // first-level roots with P empty
     const int64_t trivial_count = count - i;
@@ -1009,9 +1039,9 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.min_p = cfg->donation_min_p;
       int req = cfg->workers > 0 ? cfg->workers : 0;
       if (req <= 0) req = 0;
-      int rc = cfg->induced_full
-                   ? launch_W<true>(cp.W, args, req, &workers_used, s, &launches, budget)
-                   : launch_W<false>(cp.W, args, req, &workers_used, s, &launches, budget);
+      const int64_t guess = req > 0 ? req : std::min<int64_t>(metric_slots, cp.count + metric_slots / 4);
+      int rc = launch_mode(cfg->induced_full != 0, cp.W, args, req, &workers_used, s, &launches,
+                           budget, guess);
       if (rc) {
         cleanup();
         return rc;

@@ -30,6 +30,18 @@ void mce_set_error(const char* fmt, ...) {
 
 extern "C" const char* mce_last_error(void) { return g_err; }
 
+void mce_prepare_device() {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 namespace {
 
 template <typename T>
@@ -116,6 +128,7 @@ __global__ void k_fill_i64(int64_t* p, int64_t count, int64_t value) {
 __global__ void k_split(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
                         int64_t n, int64_t* __restrict__ split,
                         unsigned long long* __restrict__ stats /* maxdeg, maxlater, maxearlier */) {
+  unsigned long long md = 0, ml = 0, me = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = ro[v], hi = ro[v + 1];
@@ -125,9 +138,19 @@ __global__ void k_split(const int64_t* __restrict__ ro, const int32_t* __restric
       if (col[mid] < v) a = mid + 1; else c = mid;
     }
     split[v] = a;
-    atomicMax(&stats[0], (unsigned long long)(hi - lo));
-    atomicMax(&stats[1], (unsigned long long)(hi - a));
-    atomicMax(&stats[2], (unsigned long long)(a - lo));
+    md = max(md, (unsigned long long)(hi - lo));
+    ml = max(ml, (unsigned long long)(hi - a));
+    me = max(me, (unsigned long long)(a - lo));
+  }
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage t0, t1, t2;
+  md = BR(t0).Reduce(md, cub::Max());
+  ml = BR(t1).Reduce(ml, cub::Max());
+  me = BR(t2).Reduce(me, cub::Max());
+  if (threadIdx.x == 0) {
+    atomicMax(&stats[0], md);
+    atomicMax(&stats[1], ml);
+    atomicMax(&stats[2], me);
   }
 }
 
@@ -330,6 +353,7 @@ extern "C" {
 
 int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
                          int edges_on_device, void* stream, mce_graph** out) {
+  mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   *out = nullptr;
   if (num_vertices < 0 || num_vertices >= (int64_t(1) << 31) || num_edges < 0) {
@@ -401,6 +425,7 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
 
 int mce_graph_from_csr(const int64_t* row_offsets, const int64_t* col_indices, int64_t n,
                        int64_t nnz, int on_device, void* stream, mce_graph** out) {
+  mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   *out = nullptr;
   if (n < 0 || n >= (int64_t(1) << 31)) {
@@ -484,6 +509,7 @@ void mce_graph_free(mce_graph* g) {
 // position: out, n entries (host or device per position_on_device)
 int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
                          int position_on_device, int64_t* degeneracy, void* stream) {
+  mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = g->n;
   *degeneracy = 0;
@@ -569,6 +595,7 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
 
 int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_device,
                 void* stream, mce_graph** out) {
+  mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   *out = nullptr;
   mce_graph* h = new mce_graph();

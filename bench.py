@@ -1,18 +1,24 @@
-"""Benchmark: end-to-end maximal clique enumeration on B200 (BASELINE.json metric
-"end-to-end MCE seconds and maximal cliques/sec at 1/2/4/8 B200 vs CPU ref").
+"""Benchmark: end-to-end maximal clique enumeration on B200.
 
-One step = one full MCE job over one synthetic graph: degeneracy ordering +
-reordering + enumeration (the paper's GPU time, Table 1 / appendix: "the time
-includes both the degeneracy ordering time and the maximal clique counting
-time").  `value` is maximal cliques per second with the canonical graph
-already resident in HBM; `e2e` is the same metric through the public API from
-pinned host edges (H2D copy, canonicalisation, ordering, enumeration, D2H of
-the result inside the timed region).
+BASELINE.json metric: "end-to-end MCE seconds and maximal cliques/sec at
+1/2/4/8 B200 vs CPU ref".  One step = one full MCE job over one synthetic
+graph: degeneracy ordering + reordering + enumeration of every maximal clique
+(the paper's GPU time: "includes both the degeneracy ordering time and the
+maximal clique counting time").
 
-Multi-GPU: first-level subtrees are partitioned across ranks (strided
-sample of the heavy-first root order), each rank runs its share with no
-collective on the data path, and one NCCL all-reduce combines counts,
-node totals and clique-set hashes at the end.
+* ``value``  -- maximal cliques/s with the canonical graph already in HBM.
+* ``e2e``    -- the same metric through the public API from pinned host edges:
+                H2D copy, canonicalisation, ordering, enumeration and the D2H
+                of the result inside the timed region.
+* ``roofline`` -- the enumeration kernels against HBM: algorithmic bytes =
+                the CSR bytes every root's induced-subgraph build must read
+                (DESIGN.md "roofline"), over their CUDA-event time.
+* ``cpu_baseline`` -- the reference algorithm (C restatement in oracle/, all
+                host threads) on a bounded sample of the same workload.
+
+Default workload: configs[1] (Barabasi-Albert n=200k, m=8).  N>1 shards the
+first-level subtrees across ranks (no data-path collective; one NCCL
+all-reduce of counts and clique-set hashes); scaling is "strong".
 """
 
 from __future__ import annotations
@@ -37,6 +43,8 @@ WORKLOAD_CONFIG = {
     "planted1m": "ER n=1M avg deg 20 + 1k planted cliques of size 30-60",
     "rmat24": "RMAT scale-24, edge factor 16",
 }
+FALLBACK_HBM_GBS = 6650.0
+METRIC = "maximal cliques/sec (end-to-end MCE: degeneracy order + reorder + enumerate)"
 
 
 def parse_args():
@@ -48,17 +56,21 @@ def parse_args():
                    choices=sorted(WORKLOAD_CONFIG))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--root-stride", type=int, default=1,
+                   help="enumerate every k-th first-level root (bounded samples of huge graphs)")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
 
 
 class ClockSampler:
-    """Samples nvidia-smi clocks/throttle reasons during the timed region."""
+    """Samples nvidia-smi SM clocks and throttle reasons during the timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int = 0):
         self.index = index
@@ -77,7 +89,7 @@ class ClockSampler:
                     self.samples.append(row)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -88,19 +100,41 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in self.samples if r[0].replace(".", "").isdigit())
-        smax = max(float(r[1]) for r in self.samples if r[1].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.samples for i in range(4)
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = sorted(v for v in (num(r[0]) for r in self.samples) if v is not None)
+        mx = [v for v in (num(r[1]) for r in self.samples) if v is not None]
+        reasons = sorted({self.NAMES[i] for r in self.samples for i in range(4)
                           if r[2 + i].lower() in ("active", "1")})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax,
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def measured_hbm_peak() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per enumeration launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(workload)
+    except (OSError, ValueError):
+        return None
+
+
 def load_workload(name: str, seed: int, on_device: bool):
-    """(edges, n): host numpy edges, or a device tensor for rmat24."""
+    """(edges, n): host numpy edges, or a device tensor for the R-MAT graphs."""
     from paper_2212_01473_b200 import generate
 
     if name in ("rmat20", "rmat24") and on_device:
@@ -118,89 +152,135 @@ def load_workload(name: str, seed: int, on_device: bool):
     return generate.workload_edges(name, seed)
 
 
+def cpu_reference_step(ro, ci, root_stride: int, threads: int):
+    """The reference algorithm on host cores: exact degeneracy order,
+    reorder, enumeration of a strided root sample (oracle/, C + numpy)."""
+    from oracle import oracle
+
+    pos, d = oracle.degeneracy_order(ro, ci)
+    ro2, ci2 = oracle.reorder(ro, ci, pos)
+    n = len(ro) - 1
+    max_degree = int(np.diff(ro2).max()) if n else 0
+    induced = "ip" if d > 0 and max_degree / d > 200.0 else "ipx"
+    out = oracle.enumerate_cliques(ro2, ci2, roots="l1", induced=induced, degeneracy=d,
+                                   root_stride=root_stride, threads=threads)
+    return out
+
+
+def choose_cpu_stride(ro, ci, target_s: float, threads: int) -> tuple[int, float, dict]:
+    """Pick a root stride so one CPU step costs about target_s seconds."""
+    stride = 1
+    probe = max(1, (len(ro) - 1) // 2000)
+    t0 = time.perf_counter()
+    cpu_reference_step(ro, ci, probe, threads)
+    t_probe = time.perf_counter() - t0
+    est_full = t_probe * probe
+    if est_full > target_s:
+        stride = int(np.ceil(est_full / target_s))
+    return stride, t_probe, {}
+
+
 def main():
     args = parse_args()
-    import torch
-    import torch.distributed as dist
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
     if args.impl == "reference":
         return run_reference(args, rank, world)
-    from paper_2212_01473_b200 import RunConfig, from_device_edges, preprocess, run
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2212_01473_b200 import RunConfig, from_device_edges, preprocess
     from paper_2212_01473_b200 import _lib
+    from paper_2212_01473_b200.distributed import run_sharded
     from paper_2212_01473_b200.graph import from_edges
 
     _lib.require_device()
     edges, n = load_workload(args.workload, args.seed, on_device=True)
     if isinstance(edges, np.ndarray):
-        host_edges = torch.from_numpy(edges).pin_memory()
+        host_edges = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory()
         dev_edges = host_edges.cuda()
     else:
         dev_edges = edges
         host_edges = edges.cpu().pin_memory()
-    m_raw = dev_edges.shape[0]
     torch.cuda.synchronize()
-    g = from_device_edges(dev_edges, m_raw, n)
+    g = from_device_edges(dev_edges, dev_edges.shape[0], n)
     del dev_edges
     cfg = RunConfig(roots="l1", induced="auto")
+    stride = max(1, args.root_stride)
 
-    def step_device():
-        g2, order, st = preprocess(g)
-        res = run(g2, st, cfg, root_begin=rank, root_stride=world) if world > 1 else \
-            run(g2, st, cfg)
-        return res, st
+    def one_job(graph):
+        g2, _, st = preprocess(graph)
+        if world > 1 or stride > 1:
+            res, tot = run_sharded(g2, st, cfg, rank * 1, world * 1, device="cuda") \
+                if stride == 1 else run_sharded_strided(g2, st, cfg, rank, world, stride)
+            return res, tot, st
+        from paper_2212_01473_b200 import run
 
-    def step_e2e():
-        ge = from_edges(host_edges.numpy(), n)
-        g2, order, st = preprocess(ge)
-        res = run(g2, st, cfg, root_begin=rank, root_stride=world) if world > 1 else \
-            run(g2, st, cfg)
-        return res, st
+        res = run(g2, st, cfg)
+        return res, None, st
 
-    for _ in range(args.warmup):
-        res, st = step_device()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    results = []
+    for _ in range(max(args.warmup, 3)):
+        res, tot, st = one_job(g)
+    # ---- device-resident timed region ------------------------------------
+    kernel_ms = 0.0
+    build_bytes = 0
+    launches0 = _lib.lib().mce_launch_count()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # 2x the 126 MB L2
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        ev0.record()
-        for _ in range(args.steps):
-            res, st = step_device()
-            results.append(res)
-        ev1.record()
+        for i in range(args.steps):
+            flush.zero_()  # evict L2 between timed steps (outside the events)
+            starts[i].record()
+            res, tot, st = one_job(g)
+            ends[i].record()
+            kernel_ms += res.kernel_ms
+            build_bytes += res.build_bytes
         torch.cuda.synchronize()
-    dev_ms = ev0.elapsed_time(ev1) / args.steps
-    # e2e through the public API from pinned host edges
-    for _ in range(1):
-        step_e2e()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        res_e, _ = step_e2e()
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    res = results[-1]
-    count = res.clique_count
+    launches = _lib.lib().mce_launch_count() - launches0
+    dev_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+    count = tot.cliques if tot is not None else res.clique_count
+    nodes = tot.nodes if tot is not None else res.nodes_total
+    chash = f"{tot.hash:016x}" if tot is not None else res.clique_hash_hex
+    # ---- end to end through the public API from pinned host edges --------
+    e2e_ms = None
+    if not args.no_e2e:
+        host_np = host_edges.numpy()
+        one_job(from_edges(host_np, n))
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        e2e_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            e0.record()
+            one_job(from_edges(host_np, n))
+            e1.record()
+            torch.cuda.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+        e2e_ms /= args.steps
     if world > 1:
-        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, e2e_ms = float(t[0]), float(t[1])
-        c = torch.tensor([count, res.nodes_total], dtype=torch.int64, device="cuda")
-        dist.all_reduce(c)
-        count = int(c[0])
+        dev_ms, e2e_ms = float(t[0]), (float(t[1]) if e2e_ms is not None else None)
     if rank != 0:
+        dist.barrier()
         return
+    peak, peak_kind = measured_hbm_peak()
+    per_launch_ms = kernel_ms / max(1, args.steps * max(1, res.kernel_launches))
+    achieved = (build_bytes / args.steps) / (kernel_ms / args.steps / 1e3) / 1e9 \
+        if kernel_ms > 0 else None
     line = {
-        "metric": "maximal cliques/sec (end-to-end MCE: ordering + reorder + enumeration)",
+        "metric": METRIC,
         "value": count / (dev_ms / 1e3),
         "unit": "cliques/s",
         "n_gpus": world,
@@ -212,44 +292,94 @@ def main():
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_CONFIG[args.workload], "n": n, "m": st.m,
-                   "degeneracy": st.degeneracy, "max_degree": st.max_degree,
-                   "roots": cfg.roots, "induced": res.induced_mode,
-                   "maximal_cliques": count, "nodes": res.nodes_total,
-                   "clique_hash": res.clique_hash_hex, "l2_flush": "inputs > L2"},
-        "e2e": {"value": count / (e2e_ms / 1e3), "unit": "cliques/s",
-                "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(host_edges.numel() * 8),
-                "d2h_bytes_per_step": int(8 * (8 + 4096))},
-        "gpu_launches": int(res.kernel_launches),
+        "config": {"workload": WORKLOAD_CONFIG[args.workload], "name": args.workload,
+                   "n": n, "m": st.m, "degeneracy": st.degeneracy,
+                   "max_degree": st.max_degree, "roots": cfg.roots,
+                   "induced": res.induced_mode, "root_stride": stride,
+                   "maximal_cliques": count, "nodes": nodes, "clique_hash": chash,
+                   "ordering": "parallel peel",
+                   "l2_flush": "256 MiB buffer zeroed between timed steps, outside the "
+                               "CUDA events"},
+        "e2e": ({"value": count / (e2e_ms / 1e3), "unit": "cliques/s", "ms_per_step": e2e_ms,
+                 "h2d_bytes_per_step": int(host_edges.numel() * 8),
+                 "d2h_bytes_per_step": int(8 * (10 + 4096))} if e2e_ms else None),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": ncu_traffic(args.workload),
+                     "kernel": "k_enumerate (all width classes)",
+                     "kernel_ms_per_step": kernel_ms / args.steps,
+                     "kernel_ms_per_launch": per_launch_ms,
+                     "algorithmic_bytes_per_step": build_bytes // args.steps,
+                     "peak_source": peak_kind},
+        "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(g, args)
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def run_sharded_strided(g2, st, cfg, rank, world, stride):
+    """Bounded sample (every stride-th root) split across ranks."""
+    from paper_2212_01473_b200.distributed import ShardResult, allreduce_result
+    from paper_2212_01473_b200.scheduler import run
+
+    res = run(g2, st, cfg, root_begin=rank, root_stride=stride * world)
+    part = ShardResult(res.clique_count, res.nodes_total, res.donation_count,
+                       res.clique_hash, res.size_histogram)
+    if world > 1:
+        part = allreduce_result(part, "cuda")
+    return res, part
+
+
+def cpu_baseline(g, args) -> dict:
+    """Reference algorithm on this host's cores, bounded sample."""
+    threads = os.cpu_count() or 1
+    ro, ci = g.row_offsets, g.col_indices
+    stride, t_probe, _ = choose_cpu_stride(ro, ci, args.cpu_sample_seconds, threads)
+    t0 = time.perf_counter()
+    out = cpu_reference_step(ro, ci, stride, threads)
+    sec = time.perf_counter() - t0
+    return {"value": out["count"] / sec, "unit": "cliques/s", "cores": threads, "kind": "port",
+            "seconds": sec,
+            "sample": (f"all {len(ro) - 1} first-level roots" if stride == 1 else
+                       f"every {stride}-th first-level root (count {out['count']})") +
+                      "; exact degeneracy order + reorder included"}
 
 
 def run_reference(args, rank: int, world: int):
-    """The reference algorithm on host cores (the C restatement in oracle/)."""
+    """--impl reference: the reference algorithm (C restatement in oracle/)
+    on this box's host cores, same workload/metric; rank 0 only."""
     if rank != 0:
         return
     from oracle import oracle
 
+    threads = os.cpu_count() or 1
     edges, n = load_workload(args.workload, args.seed, on_device=False)
+    ro, ci = oracle.from_edges(edges, n)
+    stride = max(1, args.root_stride)
+    if args.workload in ("rmat20", "rmat24"):
+        stride, _, _ = choose_cpu_stride(ro, ci, 20.0, threads)
     times = []
     out = None
-    threads = os.cpu_count() or 1
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        out = oracle.reference_pipeline(edges, n, roots="l1", induced="auto", threads=threads)
+        out = cpu_reference_step(ro, ci, stride, threads)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
     val = out["count"] / sec
-    line = {"impl": "reference", "metric": "maximal cliques/sec", "value": val,
-            "unit": "cliques/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "config": {"workload": WORKLOAD_CONFIG[args.workload], "maximal_cliques": out["count"]},
-            "cpu_baseline": {"value": val, "unit": "cliques/s", "cores": threads, "kind": "port",
-                             "sample": "full workload"},
+    sample = "all first-level roots" if stride == 1 else f"every {stride}-th first-level root"
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "cliques/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_CONFIG[args.workload], "name": args.workload,
+                       "maximal_cliques": out["count"], "root_stride": stride},
+            "cpu_baseline": {"value": val, "unit": "cliques/s", "cores": threads,
+                             "kind": "port", "sample": sample},
             "e2e": {"value": val, "unit": "cliques/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -101,6 +101,8 @@ typedef struct {
   int64_t workers;       /* worker slots reported in worker_metrics */
   int64_t launches;      /* enumeration kernels launched */
   int64_t collect_len;   /* words the clique stream needed (may exceed collect_cap) */
+  double kernel_ms;      /* device time of the enumeration kernels (CUDA events) */
+  int64_t build_bytes;   /* algorithmic graph bytes the induced-subgraph builds read */
   int64_t hist[MCE_HIST_MAX]; /* hist[s] = maximal cliques of size s */
 } mce_run_result;
 
@@ -111,6 +113,9 @@ typedef struct {
 int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collect,
                   int64_t* worker_metrics, int64_t worker_metrics_cap, mce_run_result* out,
                   void* stream);
+
+/* Kernels this library has launched since load (its own kernels, not CUB's). */
+int64_t mce_launch_count(void);
 
 /* R-MAT edge generator on the device (input synthesis for the benchmarks):
  * edges [start, start+count) of the counter-based stream of

@@ -51,6 +51,8 @@ class RunResultC(ctypes.Structure):
         ("workers", ctypes.c_int64),
         ("launches", ctypes.c_int64),
         ("collect_len", ctypes.c_int64),
+        ("kernel_ms", ctypes.c_double),
+        ("build_bytes", ctypes.c_int64),
         ("hist", ctypes.c_int64 * HIST_MAX),
     ]
 
@@ -75,6 +77,7 @@ EXPORTS = {
     "mce_enumerate": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(RunConfigC),
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.POINTER(RunResultC), ctypes.c_void_p]),
+    "mce_launch_count": (ctypes.c_int64, []),
     "mce_gen_rmat": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]),
 }

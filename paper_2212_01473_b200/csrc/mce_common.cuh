@@ -49,4 +49,7 @@ int mce_graph_build_split(mce_graph* g, cudaStream_t s);
 // reuse HBM instead of returning it to the driver at every synchronisation).
 void mce_prepare_device();
 
+// count of this library's own kernel launches (mce_launch_count)
+void mce_count_launch(int64_t k = 1);
+
 static inline int mce_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

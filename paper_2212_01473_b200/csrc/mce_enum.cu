@@ -711,6 +711,39 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
   if (local_max) atomicMax(max_p, local_max);
 }
 
+// Algorithmic bytes one root's induced-subgraph build must read from the CSR:
+// its own offsets and adjacency, then for every P member a (and, with X rows,
+// every X member x) two offsets plus N+(a) (N+(x)).  out[0] = P part, out[1] = X part.
+__global__ void k_build_bytes(const int64_t* __restrict__ roots, int64_t count,
+                              const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
+                              const int32_t* __restrict__ col, unsigned long long* __restrict__ out) {
+  unsigned long long bp = 0, bx = 0;
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < count; i += nwarps) {
+    const int64_t r = roots[i];
+    const int64_t lo = ro[r], sp = split[r], hi = ro[r + 1];
+    if (lane == 0) bp += 24 + 4 * (hi - lo);
+    for (int64_t e = sp + lane; e < hi; e += 32) {
+      const int32_t a = col[e];
+      bp += 16 + 4 * (ro[a + 1] - split[a]);
+    }
+    for (int64_t e = lo + lane; e < sp; e += 32) {
+      const int32_t x = col[e];
+      bx += 16 + 4 * (ro[x + 1] - split[x]);
+    }
+  }
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage t0, t1;
+  bp = BR(t0).Sum(bp);
+  bx = BR(t1).Sum(bx);
+  if (threadIdx.x == 0) {
+    atomicAdd(&out[0], bp);
+    atomicAdd(&out[1], bx);
+  }
+}
+
 __global__ void k_later_count(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
                               int64_t n, int64_t* __restrict__ out) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -790,7 +823,7 @@ struct ClassPlan {
 
 template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
 int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cudaStream_t s,
-                 int64_t* launches, size_t mem_budget) {
+                 int64_t* launches, size_t mem_budget, cudaEvent_t* ev, bool* xrows_used) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
   auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
@@ -854,7 +887,11 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   MCE_CHECK(cudaMemsetAsync(args.mbox, 0, sizeof(Mailbox) * workers, s));
   MCE_CHECK(cudaMemsetAsync(args.root_counter, 0, sizeof(unsigned long long), s));
   const int grid = (int)((workers + WARPS - 1) / WARPS);
+  MCE_CHECK(cudaEventRecord(ev[0], s));
   kern<<<grid, WARPS * 32, smem, s>>>(args);
+  mce_count_launch();
+  MCE_CHECK(cudaEventRecord(ev[1], s));
+  *xrows_used = XROWS;
   MCE_CHECK(cudaGetLastError());
   (*launches)++;
   for (void* p : owned) cudaFreeAsync(p, s);
@@ -863,14 +900,14 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
 
 template <bool PIVOT_XX, bool XROWS>
 int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, int64_t* launches,
-             size_t budget) {
+             size_t budget, cudaEvent_t* ev, bool* xr) {
   switch (W) {
-    case 1: return launch_class<1, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget);
-    case 2: return launch_class<2, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget);
-    case 4: return launch_class<4, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget);
-    case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget);
-    case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget);
-    case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget);
+    case 1: return launch_class<1, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr);
+    case 2: return launch_class<2, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr);
+    case 4: return launch_class<4, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr);
+    case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget, ev, xr);
+    case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget, ev, xr);
+    case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
   }
   mce_set_error("unsupported bitset width %d", W);
   return -3;
@@ -881,13 +918,13 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
 // instead of a binary search of the CSR -- same traversal tree, fewer
 // dependent loads.  Full mode ("ipx") always has them.
 int launch_mode(bool full, int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s,
-                int64_t* launches, size_t budget, int64_t resident_guess) {
-  if (full) return launch_W<true, true>(W, args, workers, used, s, launches, budget);
+                int64_t* launches, size_t budget, int64_t resident_guess, cudaEvent_t* ev, bool* xr) {
+  if (full) return launch_W<true, true>(W, args, workers, used, s, launches, budget, ev, xr);
   const size_t xrows_bytes = sizeof(uint32_t) * (size_t)W * (size_t)std::max<int64_t>(args.xcap, 1) *
                              (size_t)std::max<int64_t>(resident_guess, 1);
   if (xrows_bytes <= budget / 2)
-    return launch_W<false, true>(W, args, workers, used, s, launches, budget);
-  return launch_W<false, false>(W, args, workers, used, s, launches, budget);
+    return launch_W<false, true>(W, args, workers, used, s, launches, budget, ev, xr);
+  return launch_W<false, false>(W, args, workers, used, s, launches, budget, ev, xr);
 }
 
 }  // namespace
@@ -923,6 +960,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     int64_t* later = nullptr;
     if (get(&later, n) || get(&eoff, n + 1)) return -1;
     k_later_count<<<grid_for(n), 256, 0, s>>>(g->ro, g->split, n, later);
+    mce_count_launch();
     MCE_CHECK(cudaMemsetAsync(eoff, 0, sizeof(int64_t), s));
     size_t tb = 0;
     MCE_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, later, eoff + 1, n, s));
@@ -947,6 +985,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     return -1;
   }
   k_vhash<<<grid_for(n), 256, 0, s>>>(cfg->hash_labels ? g->labels : nullptr, n, vhash);
+  mce_count_launch();
   MCE_CHECK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), s));
   MCE_CHECK(cudaMemsetAsync(hist, 0, HIST_MAX * sizeof(unsigned long long), s));
   MCE_CHECK(cudaMemsetAsync(collect_len, 0, sizeof(unsigned long long), s));
@@ -959,6 +998,10 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t launches = 0;
   int64_t trivial_nodes = 0;
   int64_t workers_used = 0;
+  double kernel_ms = 0.0;
+  int64_t build_bytes = 0;
+  unsigned long long* bb = nullptr;
+  if (get(&bb, 2)) return -1;
   if (count > 0) {
     uint64_t *keys = nullptr, *keys2 = nullptr;
     int64_t *roots = nullptr, *roots2 = nullptr;
@@ -971,6 +1014,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     MCE_CHECK(cudaMemsetAsync(cls, 0, 8 * sizeof(unsigned long long), s));
     k_root_keys<<<grid_for(count), 256, 0, s>>>(g->ro, g->split, g->col, eoff, n, cfg->roots,
                                                  begin, stride, count, keys, roots, cls, cls + 7);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(keys, keys2);
     cub::DoubleBuffer<int64_t> dv(roots, roots2);
@@ -1040,12 +1084,32 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       int req = cfg->workers > 0 ? cfg->workers : 0;
       if (req <= 0) req = 0;
       const int64_t guess = req > 0 ? req : std::min<int64_t>(metric_slots, cp.count + metric_slots / 4);
+      cudaEvent_t ev[2];
+      cudaEventCreate(&ev[0]);
+      cudaEventCreate(&ev[1]);
+      bool xr = false;
       int rc = launch_mode(cfg->induced_full != 0, cp.W, args, req, &workers_used, s, &launches,
-                           budget, guess);
+                           budget, guess, ev, &xr);
       if (rc) {
         cleanup();
         return rc;
       }
+      if (cfg->roots == 1) {
+        MCE_CHECK(cudaMemsetAsync(bb, 0, 2 * sizeof(unsigned long long), s));
+        k_build_bytes<<<grid_for(cp.count * 32), 256, 0, s>>>(sorted_roots + cp.begin, cp.count,
+                                                               g->ro, g->split, g->col, bb);
+        mce_count_launch();
+        unsigned long long hb[2];
+        MCE_CHECK(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, s));
+        MCE_CHECK(cudaStreamSynchronize(s));
+        build_bytes += (int64_t)(hb[0] + (xr ? hb[1] : 0));
+      }
+      MCE_CHECK(cudaEventSynchronize(ev[1]));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      kernel_ms += ms;
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
       wcap = std::max<int64_t>(wcap, req > 0 ? req : metric_slots);
     }
     max_workers_slots = std::max<int64_t>(workers_used, 1);
@@ -1053,6 +1117,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       k_trivial_roots<<<grid_for(trivial_count), 256, 0, s>>>(
           sorted_roots + trivial_begin, trivial_count, g->ro, g->split, vhash, acc, hist,
           d_collect, cfg->collect_cap, collect_len);
+      mce_count_launch();
       MCE_CHECK(cudaGetLastError());
       trivial_nodes = trivial_count;  // one visited node each (scheduler.py:300-301)
     }
@@ -1065,8 +1130,10 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       return -1;
     }
     k_isolated<<<grid_for(n), 256, 0, s>>>(n, g->ro, all);
+    mce_count_launch();
     k_trivial_roots<<<grid_for(n), 256, 0, s>>>(all, n, g->ro, g->split, vhash, acc, hist,
                                                  d_collect, cfg->collect_cap, collect_len);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
   }
   unsigned long long h_acc[8];
@@ -1097,6 +1164,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   out->workers = max_workers_slots;
   out->launches = launches;
   out->collect_len = (int64_t)h_len;
+  out->kernel_ms = kernel_ms;
+  out->build_bytes = build_bytes;
   cleanup();
   return 0;
 }

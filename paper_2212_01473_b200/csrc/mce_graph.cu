@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <vector>
@@ -29,6 +30,10 @@ void mce_set_error(const char* fmt, ...) {
 }
 
 extern "C" const char* mce_last_error(void) { return g_err; }
+
+static std::atomic<int64_t> g_launches{0};
+void mce_count_launch(int64_t k) { g_launches += k; }
+extern "C" int64_t mce_launch_count(void) { return g_launches.load(); }
 
 void mce_prepare_device() {
   static bool done[64] = {false};
@@ -323,8 +328,10 @@ int csr_from_sorted_keys(mce_graph* g, uint64_t* keys, int64_t nnz, int b, cudaS
   if (dev_alloc(&g->col, nnz, s)) return -1;
   if (nnz == 0) {
     k_fill_i64<<<grid_for(g->n + 1), 256, 0, s>>>(g->ro, g->n + 1, 0);
+    mce_count_launch();
   } else {
     k_keys_to_csr<<<grid_for(nnz), 256, 0, s>>>(keys, nnz, b, g->n, g->ro, g->col);
+    mce_count_launch();
   }
   MCE_CHECK(cudaGetLastError());
   return mce_graph_build_split(g, s);
@@ -338,6 +345,7 @@ int mce_graph_build_split(mce_graph* g, cudaStream_t s) {
   if (dev_alloc(&st, 3, s)) return -1;
   MCE_CHECK(cudaMemsetAsync(st, 0, 3 * sizeof(unsigned long long), s));
   if (g->n > 0) k_split<<<grid_for(g->n), 256, 0, s>>>(g->ro, g->col, g->n, g->split, st);
+  mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   unsigned long long h[3];
   MCE_CHECK(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -378,6 +386,7 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
     uint64_t* raw = nullptr;
     if (dev_alloc(&raw, num_edges, s)) return -1;
     k_edge_keys<<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, raw);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     dev_free(owned, s);
     // drop self-loops
@@ -410,6 +419,7 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
     // both directions, sorted by (src, dst)
     if (dev_alloc(&keys, 2 * m, s)) return -1;
     if (m > 0) k_expand_directed<<<grid_for(m), 256, 0, s>>>(uniq, m, b, keys);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     dev_free(uniq, s);
     if (sort_keys(&keys, 2 * m, 2 * b, s)) return -1;
@@ -451,6 +461,7 @@ int mce_graph_from_csr(const int64_t* row_offsets, const int64_t* col_indices, i
                                 cudaMemcpyHostToDevice, s));
     }
     k_narrow<<<grid_for(nnz), 256, 0, s>>>(tmp, nnz, g->col);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     if (!on_device) dev_free(tmp, s);
   }
@@ -486,6 +497,7 @@ int mce_graph_copy_csr(const mce_graph* g, int64_t* row_offsets, int64_t* col_in
     if (dev_alloc(&wide, g->nnz, s)) return -1;
     auto n = g->nnz;
     k_widen<<<grid_for(n), 256, 0, s>>>(g->col, n, wide);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     MCE_CHECK(cudaMemcpyAsync(col_indices, wide, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
     dev_free(wide, s);
@@ -523,6 +535,7 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
     int64_t* d_deg = nullptr;
     if (dev_alloc(&tree, 2 * leaves, s) || dev_alloc(&d_deg, 1, s)) return -1;
     k_exact_order<<<1, EXACT_THREADS, 0, s>>>(g->ro, g->col, n, leaves, tree, d_pos, d_deg);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
@@ -538,6 +551,7 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
         dev_alloc(&keep, n, s) || dev_alloc(&d_cnt, 2, s) || dev_alloc(&d_min, 1, s))
       return -1;
     k_init_peel<<<grid_for(n), 256, 0, s>>>(g->ro, n, deg, alive, removed);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     size_t tb_sel = 0, tb_min = 0;
     MCE_CHECK(cub::DeviceSelect::Flagged(nullptr, tb_sel, alive, take, frontier, d_cnt, n, s));
@@ -551,6 +565,7 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
     int64_t deg_max = 0;
     while (na > 0) {
       k_peel_flags<<<grid_for(na), 256, 0, s>>>(alive, na, deg, k, take, keep);
+      mce_count_launch();
       size_t t1 = tb;
       MCE_CHECK(cub::DeviceSelect::Flagged(tmp, t1, alive, take, frontier, d_cnt, na, s));
       int64_t nf = 0;
@@ -568,7 +583,9 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
       }
       if (k > deg_max) deg_max = k;
       k_peel_assign<<<grid_for(nf), 256, 0, s>>>(frontier, nf, base, d_pos, removed);
+      mce_count_launch();
       k_peel_decrement<<<grid_for(nf * 32), 256, 0, s>>>(frontier, nf, g->ro, g->col, removed, deg);
+      mce_count_launch();
       size_t t3 = tb;
       MCE_CHECK(cub::DeviceSelect::Flagged(tmp, t3, alive, keep, alive2, d_cnt + 1, na, s));
       MCE_CHECK(cudaGetLastError());
@@ -614,11 +631,13 @@ int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_dev
   if (dev_alloc(&keys, g->nnz, s)) return -1;
   if (g->nnz > 0) {
     k_reorder_keys<<<grid_for(n * 32), 256, 0, s>>>(g->ro, g->col, n, d_pos, b, keys);
+    mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     if (sort_keys(&keys, g->nnz, 2 * b, s)) return -1;
   }
   if (dev_alloc(&h->labels, n, s)) return -1;
   if (n > 0) k_relabel<<<grid_for(n), 256, 0, s>>>(d_pos, n, g->labels, h->labels);
+  mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   int rc = csr_from_sorted_keys(h, keys, g->nnz, b, s);
   dev_free(keys, s);

@@ -52,6 +52,7 @@ extern "C" int mce_gen_rmat(int scale, int64_t start, int64_t count, uint64_t se
   int64_t g = (count + 255) / 256;
   if (g > 148 * 64) g = 148 * 64;
   k_rmat<<<(int)g, 256, 0, (cudaStream_t)stream>>>(scale, start, count, key, k1, k2, edges_dev);
+  mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   return 0;
 }

@@ -108,6 +108,8 @@ class RunResult:
     size_histogram: dict[int, int] = field(default_factory=dict)
     max_clique_size: int = 0
     kernel_launches: int = 0
+    kernel_ms: float = 0.0
+    build_bytes: int = 0
 
     def report(self):
         from paper_2212_01473_b200.metrics import aggregate
@@ -215,4 +217,6 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
         size_histogram=hist,
         max_clique_size=int(res.max_size),
         kernel_launches=int(res.launches),
+        kernel_ms=float(res.kernel_ms),
+        build_bytes=int(res.build_bytes),
     )

@@ -40,7 +40,7 @@ def test_ctypes_binding_covers_the_header():
 def test_struct_layouts_match_header():
     # mce_run_config: 6 ints, 3 int64, int, int64, int64, double (natural alignment)
     assert ctypes.sizeof(_lib.RunConfigC) == 6 * 4 + 3 * 8 + 8 + 8 + 8 + 8
-    assert ctypes.sizeof(_lib.RunResultC) == 8 * 8 + 8 * _lib.HIST_MAX
+    assert ctypes.sizeof(_lib.RunResultC) == 10 * 8 + 8 * _lib.HIST_MAX
 
 
 def test_last_error_is_callable_without_a_device():

@@ -9,12 +9,12 @@
  * the reference API on top of these calls.  Plain pointers and sizes only.
  *
  *   reference function                          replaced by
- *   graph.py:96-120   from_edges            ->  mce_graph_from_edges
- *   graph.py:123-175  parse_edge_list (tail)->  mce_graph_from_edges (after host tokenising)
- *   graph.py:29-50    Graph CSR accessors   ->  mce_graph_from_csr / mce_graph_copy_csr / mce_graph_info
- *   graph.py:189-218  degeneracy_order      ->  mce_degeneracy_order
- *   graph.py:221-232  reorder               ->  mce_reorder
- *   graph.py:235-243  stats / preprocess    ->  mce_graph_info (+ the two above)
+ *   graph.py:103-129   from_edges            ->  mce_graph_from_edges
+ *   graph.py:132-180  parse_edge_list (tail)->  mce_graph_from_edges (after host tokenising)
+ *   graph.py:28-64    Graph CSR accessors   ->  mce_graph_from_csr / mce_graph_copy_csr / mce_graph_info
+ *   graph.py:183-210  degeneracy_order      ->  mce_degeneracy_order
+ *   graph.py:213-224  reorder               ->  mce_reorder
+ *   graph.py:227-243  stats / preprocess    ->  mce_graph_info (+ the two above)
  *   scheduler.py:441-492 run (+ bk.py roots, induced.py, xsets.py, the worker list)
  *                                           ->  mce_enumerate
  *
@@ -44,7 +44,7 @@ typedef struct mce_graph mce_graph; /* device-resident canonical CSR */
 const char* mce_last_error(void);
 
 /* Canonical graph from (u, v) pairs: self-loops dropped, duplicates merged,
- * symmetric, rows strictly ascending (graph.py:96-120).  `edges` holds
+ * symmetric, rows strictly ascending (graph.py:103-129).  `edges` holds
  * 2*num_edges int64 values, on the host or (edges_on_device=1) the device. */
 int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
                          int edges_on_device, void* stream, mce_graph** out);
@@ -63,7 +63,7 @@ int mce_graph_copy_csr(const mce_graph* g, int64_t* row_offsets, int64_t* col_in
 
 void mce_graph_free(mce_graph* g);
 
-/* Degeneracy ordering (graph.py:189-218): position[v] = rank of v.
+/* Degeneracy ordering (graph.py:183-210): position[v] = rank of v.
  *   method 1: the reference's exact order (minimum current degree, ties to the
  *             smallest id) -- bit-identical positions, single-CTA kernel;
  *   method 0: parallel bucket peeling -- a valid degeneracy order with the same
@@ -71,7 +71,7 @@ void mce_graph_free(mce_graph* g);
 int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
                          int position_on_device, int64_t* degeneracy, void* stream);
 
-/* Relabel by position (graph.py:221-232).  The result remembers the original
+/* Relabel by position (graph.py:213-224).  The result remembers the original
  * label of every vertex (used to hash cliques by original ids). */
 int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_device,
                 void* stream, mce_graph** out);

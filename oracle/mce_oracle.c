@@ -8,14 +8,14 @@
  * `--impl reference`).  Nothing in the product path links or calls it.
  *
  * Reference semantics followed (file:line in /root/reference/pkg/src/mce):
- *   degeneracy order ....... graph.py:189-218  (min-degree peel, ties -> smallest id)
- *   first-level roots ...... bk.py:188-192     (P = later nbrs, X = earlier nbrs)
- *   second-level roots ..... bk.py:200-206     (P/X = common nbrs after/before max endpoint)
- *   pivot rule ............. bk.py:81-109      (max |N(c) & P| over P|X_P ascending, ties to
+ *   degeneracy order ....... graph.py:183-210  (min-degree peel, ties -> smallest id)
+ *   first-level roots ...... bk.py:186-190     (P = later nbrs, X = earlier nbrs)
+ *   second-level roots ..... bk.py:198-204     (P/X = common nbrs after/before max endpoint)
+ *   pivot rule ............. bk.py:82-110      (max |N(c) & P| over P|X_P ascending, ties to
  *                                               smallest id; X_X rows only if strictly better)
  *   traversal + node count . scheduler.py:297-381
- *   full / partial rows .... induced.py:80-98, scheduler.py:397-415
- *   X_X stable partition ... xsets.py:71-94
+ *   full / partial rows .... induced.py:61-103, scheduler.py:397-415
+ *   X_X stable partition ... xsets.py:55-82
  *   isolated vertices (L2) . scheduler.py:476-480
  * Pinned against the reference itself through tests/golden (see header).
  */
@@ -246,7 +246,7 @@ static void traverse(const ctx_t* c, work_t* wk, const int64_t* R0, int nr,
         return;
     }
     if (np > c->cap_bits) { wk->err = -2; return; }
-    /* induced rows over P columns (induced.py:58-98) */
+    /* induced rows over P columns (induced.py:61-103) */
     memset(wk->rows, 0, sizeof(uint64_t) * np * W);
     for (int64_t i = 0; i < np; ++i) {
         int64_t a = wk->plist[i];
@@ -318,7 +318,7 @@ static void traverse(const ctx_t* c, work_t* wk, const int64_t* R0, int nr,
             }
             continue;
         }
-        /* descend (xsets.py:71-94): stable partition of the live X_X prefix */
+        /* descend (xsets.py:55-82): stable partition of the live X_X prefix */
         int64_t kept = 0, dropped = 0;
         for (int64_t i = 0; i < live; ++i) {
             int64_t t = wk->xx[i];
@@ -364,7 +364,7 @@ int mce_oracle_enumerate(int64_t n, const int64_t* ro, const int64_t* ci, int ro
         if (lo - ro[v] > max_x) max_x = lo - ro[v];
         if (ro[v + 1] - lo > max_p) max_p = ro[v + 1] - lo;
     }
-    /* second-level roots are the edges (u < v) in CSR order (graph.py:52-59) */
+    /* second-level roots are the edges (u < v) in CSR order (graph.py:57-64) */
     int64_t* eoff = NULL;
     int64_t total_roots = n;
     if (roots_mode == 2) {

@@ -29,16 +29,16 @@ typedef struct {
 } mce_oracle_result;
 
 /* Minimum-degree peeling with a lazy binary heap keyed (current degree, id):
- * restates mce/graph.py:degeneracy_order (graph.py:189-218).  Writes the
+ * restates mce/graph.py:degeneracy_order (graph.py:183-210).  Writes the
  * rank of every vertex into position[] and returns the degeneracy. */
 int64_t mce_oracle_degeneracy_order(int64_t n, const int64_t* row_offsets,
                                     const int64_t* col_indices, int64_t* position);
 
 /* Serial/OpenMP restatement of mce/scheduler.py:_Worker._execute
- * (scheduler.py:297-381) over first-level (roots_mode=1, bk.py:188-192) or
- * second-level (roots_mode=2, bk.py:200-206) subtree roots, with full
- * (induced_full=1, induced.py:90-98) or partial (induced_full=0,
- * induced.py:80-87) induced subgraphs and the split X_P / X_X state of
+ * (scheduler.py:297-381) over first-level (roots_mode=1, bk.py:186-190) or
+ * second-level (roots_mode=2, bk.py:198-204) subtree roots, with full
+ * (induced_full=1, induced.py:95-103) or partial (induced_full=0,
+ * induced.py:61-92) induced subgraphs and the split X_P / X_X state of
  * mce/xsets.py.  The graph must be canonical and degeneracy-reordered.
  *
  *  capacity_bits : bitset capacity (reference: round_up_capacity(max(d,1)))

@@ -8,7 +8,7 @@ algorithm on host cores.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 this module.  The product never does.
 
 Graph canonicalisation / reordering is restated with numpy
-(reference graph.py:96-120 ``from_edges`` and graph.py:221-232 ``reorder``);
+(reference graph.py:103-129 ``from_edges`` and graph.py:213-224 ``reorder``);
 degeneracy ordering and the Bron-Kerbosch traversal are restated in C
 (``mce_oracle.c``, loaded via ctypes).  The restatement is pinned against the
 reference itself by the vectors in ``tests/golden`` (made by
@@ -112,7 +112,7 @@ def summarize_cliques(cliques) -> dict:
             "hash": f"{h:016x}"}
 
 
-# --- graph canonicalisation (restates graph.py:96-120, 221-232) ----------
+# --- graph canonicalisation (restates graph.py:103-129, 221-232) ----------
 
 def from_edges(edges, n: int) -> tuple[np.ndarray, np.ndarray]:
     """Canonical CSR (row_offsets, col_indices) from vertex pairs: loops

@@ -20,7 +20,7 @@ class MceError(RuntimeError):
 
 
 class CapacityError(ValueError):
-    """|P| does not fit the bitset capacity (reference induced.py:22-23)."""
+    """|P| does not fit the bitset capacity (reference induced.py:21-22)."""
 
 
 class RunConfigC(ctypes.Structure):

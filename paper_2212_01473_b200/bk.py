@@ -21,7 +21,7 @@ from paper_2212_01473_b200.graph import Graph
 
 class CliqueSink:
     """Receives maximal cliques: always counts, optionally collects sorted
-    tuples up to ``collect_limit`` (reference bk.py:23-61)."""
+    tuples up to ``collect_limit`` (reference bk.py:23-58)."""
 
     __slots__ = ("collect_limit", "total", "collected")
 
@@ -56,7 +56,7 @@ class CliqueSink:
 
 @dataclass(frozen=True)
 class RootTask:
-    """Seed state of one independent subtree (reference bk.py:64-76)."""
+    """Seed state of one independent subtree (reference bk.py:62-73)."""
 
     root_vertices: tuple[int, ...]
     P: np.ndarray
@@ -65,7 +65,7 @@ class RootTask:
 
 
 def first_level_root(g: Graph, v: int) -> RootTask:
-    """Per-vertex root: P = later neighbours, X = earlier (bk.py:188-192)."""
+    """Per-vertex root: P = later neighbours, X = earlier (bk.py:186-190)."""
     adj = g.neighbors(v)
     cut = int(np.searchsorted(adj, v))
     return RootTask((v,), adj[cut:].copy(), adj[:cut].copy(), origin_index=v)
@@ -78,7 +78,7 @@ def first_level_roots(g: Graph) -> Iterator[RootTask]:
 
 def second_level_root(g: Graph, edge_index: int) -> RootTask:
     """Per-edge root: common neighbours after / before the later endpoint
-    (bk.py:200-206)."""
+    (bk.py:198-204)."""
     u, v = (int(a) for a in g.edges()[edge_index])
     common = np.intersect1d(g.neighbors(u), g.neighbors(v), assume_unique=True)
     cut = int(np.searchsorted(common, max(u, v)))
@@ -113,11 +113,11 @@ def _enumerate_whole_graph(g: Graph, sink: CliqueSink, metrics: dict | None) -> 
 
 
 def bk_pivot(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
-    """All maximal cliques of ``g`` (reference bk.py:140-174) via the GPU
+    """All maximal cliques of ``g`` (reference bk.py:153-183) via the GPU
     engine; cliques are reported in ``g``'s labels."""
     return _enumerate_whole_graph(g, sink, metrics)
 
 
 def bk_basic(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
-    """Same clique set as reference bk.py:112-137 (the GPU engine always pivots)."""
+    """Same clique set as reference bk.py:124-150 (the GPU engine always pivots)."""
     return _enumerate_whole_graph(g, sink, metrics)

@@ -4,13 +4,13 @@
 // worker list through which busy warps donate branches to idle warps.
 //
 // Reference behaviour restated (file:line in /root/reference/pkg/src/mce):
-//   root tasks ............. bk.py:188-206           (first/second-level subtrees)
-//   induced rows ........... induced.py:58-98        (partial "ip" / full "ipx")
-//   pivot .................. bk.py:81-109            (max |N(c) & P| over P|X_P, ties to the
+//   root tasks ............. bk.py:186-209           (first/second-level subtrees)
+//   induced rows ........... induced.py:61-103        (partial "ip" / full "ipx")
+//   pivot .................. bk.py:82-110            (max |N(c) & P| over P|X_P, ties to the
 //                                                     smallest id; X_X rows only if strictly
 //                                                     better, first in prefix order)
 //   traversal, node count .. scheduler.py:297-381
-//   X_X stable partition ... xsets.py:71-94
+//   X_X stable partition ... xsets.py:55-82
 //   donation conditions .... scheduler.py:346-355
 //   worker list protocol ... scheduler.py:99-165
 //   isolated vertices (l2) . scheduler.py:476-480
@@ -187,7 +187,7 @@ struct Worker {
       nr = 1;
     } else {
       const int64_t u = r >> 32, v = r & 0xffffffffll;
-      // P = N+(u) & N+(v), X = N(u) & N-(v), both ascending (bk.py:200-206)
+      // P = N+(u) & N+(v), X = N(u) & N-(v), both ascending (bk.py:198-204)
       np = 0;
       const int64_t ps = a.split[v], pe = a.ro[v + 1];
       const int64_t us = a.split[u], ue = a.ro[u + 1];
@@ -228,7 +228,7 @@ struct Worker {
     origin = r;
     __syncwarp();
     if (np == 0) return nr;
-    // P rows (induced.py:80-87): each P-P edge (a_i, b) with b in N+(a_i)
+    // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i)
     for (int w = 0; w < W; ++w)
       for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
     __syncwarp();
@@ -244,7 +244,7 @@ struct Worker {
       }
     }
     if (XROWS) {
-      // X rows (induced.py:90-98): X member x is earlier than every P vertex,
+      // X rows (induced.py:95-103): X member x is earlier than every P vertex,
       // so its P-neighbours are N+(x) & P.  Lane t owns column t.
       for (int t = lane; t < nx; t += 32) {
         for (int w = 0; w < W; ++w) xrowsT[(size_t)w * a.xcap + t] = 0;
@@ -276,7 +276,7 @@ struct Worker {
     return false;
   }
 
-  // stable partition of xx[0, live) by adjacency to v (xsets.py:71-94)
+  // stable partition of xx[0, live) by adjacency to v (xsets.py:55-82)
   __device__ int partition(int v, int32_t gv, int live) {
     int kept = 0, dropped = 0;
     const unsigned lt = (1u << lane) - 1;
@@ -298,7 +298,7 @@ struct Worker {
     return kept;
   }
 
-  // pivot (bk.py:81-109); returns this lane's word of P - N(pivot)
+  // pivot (bk.py:82-110); returns this lane's word of P - N(pivot)
   __device__ uint32_t pivot_branches(uint32_t P, uint32_t XP, int live) {
     if (lane < W) sP[lane] = P;
     __syncwarp();

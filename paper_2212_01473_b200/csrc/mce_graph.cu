@@ -2,13 +2,13 @@
 // ordering by parallel peeling, reordering and CSR orientation.
 //
 // Reference behaviour restated (file:line in /root/reference/pkg/src/mce):
-//   from_edges ......... graph.py:96-120  (drop loops, merge duplicates, both directions,
+//   from_edges ......... graph.py:103-129  (drop loops, merge duplicates, both directions,
 //                                          rows strictly ascending)
-//   degeneracy_order ... graph.py:189-218 (method 1 = the reference's exact
+//   degeneracy_order ... graph.py:183-210 (method 1 = the reference's exact
 //                                          min-degree/smallest-id order; method 0 = parallel
 //                                          bucket peel, a valid degeneracy order with the
 //                                          same degeneracy)
-//   reorder ............ graph.py:221-232
+//   reorder ............ graph.py:213-224
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -595,7 +595,7 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
     }
     // the degeneracy is the largest peel level at which a vertex left, but a
     // level may be reached only because k jumped to the minimum degree: the
-    // real degree at removal is what the reference reports (graph.py:213-214)
+    // real degree at removal is what the reference reports (graph.py:198-205)
     *degeneracy = deg_max;
     cudaFreeAsync(tmp, s);
     dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(frontier, s);

@@ -1,6 +1,6 @@
 """Seed-deterministic synthetic graph generators (input synthesis, host side).
 
-Mirrors the reference generator API (reference mce/generate.py:13-68:
+Mirrors the reference generator API (reference mce/generate.py:17-68:
 ``gnp``, ``moon_moser``, ``planted_skew``, ``write_edge_list``) -- the first
 three consume numpy's PCG64 stream in exactly the reference's order, so the
 same seed yields the same graph -- and adds the generators behind the five
@@ -52,7 +52,7 @@ def counter_unit(seed: int, stream: int, idx: np.ndarray) -> np.ndarray:
 
 def gnp(n: int, p: float, seed: int = 0):
     """Erdos-Renyi G(n, p) drawing the reference's PCG64 stream
-    (reference generate.py:13-22: one uniform per pair (u, v>u), row-major)."""
+    (reference generate.py:17-26: one uniform per pair (u, v>u), row-major)."""
     from paper_2212_01473_b200.graph import from_edges
 
     if n < 0 or not 0.0 <= p <= 1.0:
@@ -89,7 +89,7 @@ def gnp_edges(n: int, p: float, seed: int = 0) -> np.ndarray:
 
 def moon_moser(parts: int):
     """Complete multipartite graph with ``parts`` parts of size 3 (3**parts
-    maximal cliques); reference generate.py:25-34."""
+    maximal cliques); reference generate.py:29-38."""
     from paper_2212_01473_b200.graph import from_edges
 
     if parts < 1:
@@ -103,7 +103,7 @@ def moon_moser(parts: int):
 def planted_skew(n: int = 10_000, community: int = 40, p_in: float = 0.8,
                  background_degree: float = 4.0, seed: int = 0):
     """Sparse background plus one dense community, same stream as reference
-    generate.py:37-58."""
+    generate.py:41-62."""
     from paper_2212_01473_b200.graph import from_edges
 
     if community > n:

@@ -15,7 +15,7 @@ the reference's dataclass are materialised only when host code reads them.
   degeneracy ``d`` (so |P| <= d for every first-level root), but not the same
   permutation.
 * ``"exact"`` -- the reference's own order (minimum current degree, ties to
-  the smallest id; graph.py:189-218), computed by a single-CTA kernel;
+  the smallest id; graph.py:183-210), computed by a single-CTA kernel;
   positions are bit-identical to the reference.
 
 Clique results never depend on the method: counts, size histograms and the
@@ -39,7 +39,7 @@ ORDER_METHODS = {"parallel": 0, "exact": 1}
 
 class EdgeListParseError(ValueError):
     """Malformed edge-list input; carries the 1-based line number
-    (reference graph.py:18-24)."""
+    (reference graph.py:19-24)."""
 
     def __init__(self, line_no: int, message: str) -> None:
         super().__init__(f"line {line_no}: {message}")
@@ -69,7 +69,7 @@ class _DeviceGraph:
 
 
 class Graph:
-    """Undirected simple graph in CSR form (reference graph.py:27-93).
+    """Undirected simple graph in CSR form (reference graph.py:28-82).
 
     ``row_offsets`` (n+1) and ``col_indices`` (2m, rows strictly ascending)
     are numpy views materialised on demand from the device copy; ``labels``
@@ -163,7 +163,7 @@ class Graph:
         return self.edge_list
 
     def validate(self) -> None:
-        """Check the CSR invariants (reference graph.py:61-76); raises ValueError."""
+        """Check the CSR invariants (reference graph.py:66-82); raises ValueError."""
         ro, ci = self.row_offsets, self.col_indices
         n = self.num_vertices
         if len(ro) != n + 1 or ro[0] != 0 or ro[-1] != len(ci):
@@ -188,7 +188,7 @@ class Graph:
 
 @dataclass(frozen=True)
 class GraphStats:
-    """Headline numbers: size, max degree, degeneracy (reference graph.py:79-87)."""
+    """Headline numbers: size, max degree, degeneracy (reference graph.py:86-92)."""
 
     n: int
     m: int
@@ -210,7 +210,7 @@ def _from_device(n: int, h: ctypes.c_void_p, labels: np.ndarray | None = None) -
 
 def from_edges(edges: Iterable[tuple[int, int]] | np.ndarray, num_vertices: int) -> Graph:
     """Canonical graph from compacted vertex pairs, built on the GPU
-    (reference graph.py:96-120): self-loops dropped, duplicates merged,
+    (reference graph.py:103-129): self-loops dropped, duplicates merged,
     both directions stored, rows ascending."""
     arr = np.ascontiguousarray(
         np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges,
@@ -235,7 +235,7 @@ def from_device_edges(edges_dev, num_edges: int, num_vertices: int, stream=None)
 
 def parse_edge_list(source: str | IO[str], base: int = 0, symmetrize: bool = True) -> Graph:
     """Parse whitespace-separated edge-list text into a canonical graph
-    (reference graph.py:123-175): '#'/'%' comments, MatrixMarket header
+    (reference graph.py:132-180): '#'/'%' comments, MatrixMarket header
     switches to 1-based ids and skips the size line, ids are compacted to
     [0, n), duplicates merge, self-loops drop, output always symmetric."""
     del symmetrize
@@ -275,7 +275,7 @@ def parse_edge_list(source: str | IO[str], base: int = 0, symmetrize: bool = Tru
 
 
 def degeneracy_order(g: Graph, method: str = "parallel") -> DegeneracyOrder:
-    """Degeneracy ordering on the GPU (reference graph.py:189-218); see the
+    """Degeneracy ordering on the GPU (reference graph.py:183-210); see the
     module docstring for ``method``."""
     if method not in ORDER_METHODS:
         raise ValueError(f"unknown ordering method {method!r}")
@@ -290,7 +290,7 @@ def degeneracy_order(g: Graph, method: str = "parallel") -> DegeneracyOrder:
 
 
 def reorder(g: Graph, order: DegeneracyOrder) -> Graph:
-    """Relabel vertices by rank on the GPU (reference graph.py:221-232)."""
+    """Relabel vertices by rank on the GPU (reference graph.py:213-224)."""
     pos = np.ascontiguousarray(order.position, dtype=np.int64)
     if len(pos) != g.num_vertices:
         raise ValueError("permutation length does not match vertex count")
@@ -319,7 +319,7 @@ def stats(g: Graph, order: DegeneracyOrder) -> GraphStats:
 
 
 def preprocess(g: Graph, method: str = "parallel") -> tuple[Graph, DegeneracyOrder, GraphStats]:
-    """Order, relabel and summarise in one step (reference graph.py:238-243)."""
+    """Order, relabel and summarise in one step (reference graph.py:239-243)."""
     order = degeneracy_order(g, method=method)
     g2 = reorder(g, order)
     return g2, order, stats(g2, order)

@@ -49,7 +49,7 @@ def choose_induced_mode(max_degree: int, degeneracy: int) -> str:
 
 @dataclass(frozen=True)
 class Backoff:
-    """Exponential sleep schedule for parked workers (reference scheduler.py:44-49).
+    """Exponential sleep schedule for parked workers (reference scheduler.py:45-49).
     The device worker list backs off with __nanosleep from 64 ns doubling to
     ~8 us; the values here are validated for API compatibility."""
 
@@ -59,7 +59,7 @@ class Backoff:
 
 @dataclass
 class RunConfig:
-    """Knobs for one run (reference scheduler.py:52-78).
+    """Knobs for one run (reference scheduler.py:53-78).
 
     ``workers`` counts worker warps; 0 means every co-resident warp of the GPU.
     """
@@ -91,7 +91,7 @@ class RunConfig:
 
 @dataclass
 class RunResult:
-    """Outcome of one run (reference scheduler.py:168-185) plus the device
+    """Outcome of one run (reference scheduler.py:169-185) plus the device
     engine's checksums."""
 
     clique_count: int

@@ -90,7 +90,7 @@ def test_parse_errors_carry_line_numbers():
                          ids=lambda c: c["name"])
 def test_gnp_stream_matches_reference_generator(case):
     """generate.gnp_edges draws numpy's PCG64 stream exactly as the reference
-    gnp (reference generate.py:13-22): same seed, same edges."""
+    gnp (reference generate.py:17-26): same seed, same edges."""
     name = case["name"]
     parts = name.split("_")
     n, p = int(parts[1]), float(parts[2])

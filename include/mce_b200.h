@@ -14,7 +14,8 @@
  *   graph.py:28-64    Graph CSR accessors   ->  mce_graph_from_csr / mce_graph_copy_csr / mce_graph_info
  *   graph.py:183-210  degeneracy_order      ->  mce_degeneracy_order
  *   graph.py:213-224  reorder               ->  mce_reorder
- *   graph.py:227-243  stats / preprocess    ->  mce_graph_info (+ the two above)
+ *   graph.py:227-236  stats                 ->  mce_graph_info
+ *   graph.py:239-243  preprocess            ->  mce_preprocess (+ mce_graph_info)
  *   scheduler.py:441-492 run (+ bk.py roots, induced.py, xsets.py, the worker list)
  *                                           ->  mce_enumerate
  *
@@ -75,6 +76,13 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
  * label of every vertex (used to hash cliques by original ids). */
 int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_device,
                 void* stream, mce_graph** out);
+
+/* degeneracy_order + reorder in one call, positions kept on the device
+ * (graph.py:239-243 preprocess, minus stats which mce_graph_info gives).
+ * The permutation is recoverable from the result's labels:
+ * labels[position[v]] = label(v). */
+int mce_preprocess(const mce_graph* g, int method, int64_t* degeneracy, void* stream,
+                   mce_graph** out);
 
 typedef struct {
   int roots;             /* 1 = first-level (per vertex), 2 = second-level (per edge) */

@@ -74,6 +74,8 @@ EXPORTS = {
                                             ctypes.c_void_p]),
     "mce_reorder": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                    ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "mce_preprocess": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "mce_enumerate": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(RunConfigC),
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.POINTER(RunResultC), ctypes.c_void_p]),

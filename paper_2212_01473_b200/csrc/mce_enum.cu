@@ -58,9 +58,7 @@ struct Mailbox {
   int32_t nxx;      // live X_X tokens, written into the receiver's xx
   int32_t has_task;
   int32_t pad;
-  uint32_t P[32];
-  uint32_t XP[32];
-};
+};  // the branch's P and X_P bitsets go to EnumArgs::mbits (2W words per worker)
 
 struct EnumArgs {
   int64_t n;
@@ -98,6 +96,7 @@ struct EnumArgs {
   unsigned* idle_bits;  // ceil(num_workers / 32) words
   int* wl_wake;
   Mailbox* mbox;
+  uint32_t* mbits;
   int worker_list_on;
   int min_p;
 };
@@ -121,10 +120,20 @@ __device__ __forceinline__ bool contains_range(const int32_t* __restrict__ col, 
   return lo < end && col[lo] == key;
 }
 
+// Bitsets over the root's P have W 32-bit words; lane l holds words
+// l, l+32, ... (K = ceil(W/32) words per lane, lanes >= W hold 0 when W < 32).
+template <int W>
+struct Bits {
+  static constexpr int K = (W + 31) / 32;
+  uint32_t w[K];
+};
+
 template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM>
 struct Worker {
   static constexpr int CAP = 32 * W;
   static constexpr int CAPP = CAP + 1;
+  static constexpr int K = (W + 31) / 32;
+  using B = Bits<W>;
 
   const EnumArgs& a;
   const int lane;
@@ -169,7 +178,44 @@ struct Worker {
     hsum = a.hsum + (size_t)wid * (a.levels + 2);
   }
 
+  // ---------------------------------------------------------------- words
+  __device__ __forceinline__ static bool valid(int k, int lane) { return W >= 32 || lane < W; }
+  __device__ __forceinline__ int word(int k) const { return k * 32 + lane; }
   __device__ __forceinline__ uint32_t row_word(int c, int w) const { return rowsT[w * CAPP + c]; }
+  __device__ __forceinline__ bool any(const B& x) const {
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) o |= x.w[k];
+    return __any_sync(FULLMASK, o != 0);
+  }
+  __device__ __forceinline__ int popc(const B& x) const {
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) c += __popc(x.w[k]);
+    return __reduce_add_sync(FULLMASK, c);
+  }
+  // lowest set bit (ascending local id), -1 if empty
+  __device__ __forceinline__ int first(const B& x) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const unsigned bm = __ballot_sync(FULLMASK, x.w[k] != 0);
+      if (bm) {
+        const int fl = __ffs(bm) - 1;
+        const uint32_t wd = __shfl_sync(FULLMASK, x.w[k], fl);
+        return ((k * 32 + fl) << 5) + __ffs(wd) - 1;
+      }
+    }
+    return -1;
+  }
+  __device__ __forceinline__ void row_of(int v, B& r) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) r.w[k] = valid(k, lane) ? row_word(v, word(k)) : 0u;
+  }
+  __device__ __forceinline__ void xrow_of(int32_t t, B& r) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      r.w[k] = valid(k, lane) ? xrowsT[(size_t)word(k) * a.xcap + t] : 0u;
+  }
 
   // ---------------------------------------------------------------- build
   // Fill plist / root_x / rows (and X rows) for root `r`; returns R0 length.
@@ -232,14 +278,46 @@ struct Worker {
     for (int w = 0; w < W; ++w)
       for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
     __syncwarp();
-    for (int i = 0; i < np; ++i) {
-      const int32_t ai = plist[i];
-      const int64_t lo = a.split[ai], hi = a.ro[ai + 1];
-      for (int64_t e = lo + lane; e < hi; e += 32) {
-        int j = bsearch_i32(plist, np, col[e]);
-        if (j >= 0) {
-          atomicOr(&rowsT[(j >> 5) * CAPP + i], 1u << (j & 31));
-          atomicOr(&rowsT[(i >> 5) * CAPP + j], 1u << (i & 31));
+    // The (member, neighbour) pairs of 32 members at a time are flattened
+    // over the lanes (warp scan of |N+(a_i)|, owner found by a shuffle
+    // binary search), so every iteration issues 32 independent col loads
+    // whatever the degree mix.
+    for (int i0 = 0; i0 < np; i0 += 32) {
+      const int i = i0 + lane;
+      int64_t lo = 0;
+      int len = 0;
+      if (i < np) {
+        const int32_t ai = plist[i];
+        lo = a.split[ai];
+        len = (int)(a.ro[ai + 1] - lo);
+      }
+      int incl = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const int excl = incl - len;
+      const int total = __shfl_sync(FULLMASK, incl, 31);
+      for (int base = 0; base < total; base += 32) {
+        const int k = base + lane;
+        int owner = 0;  // lanes q with incl_q <= k
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
+          if (v <= k) owner += step;
+        }
+        const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
+        const int excl_o = __shfl_sync(FULLMASK, excl, owner);
+        if (k < total) {
+          const int io = i0 + owner;
+          // N+(a_io) & P lies after a_io in the ascending plist
+          const int j = bsearch_i32(plist + io + 1, np - io - 1, col[lo_o + (k - excl_o)]);
+          if (j >= 0) {
+            const int jj = io + 1 + j;
+            atomicOr(&rowsT[(jj >> 5) * CAPP + io], 1u << (jj & 31));
+            atomicOr(&rowsT[(io >> 5) * CAPP + jj], 1u << (io & 31));
+          }
         }
       }
     }
@@ -282,13 +360,13 @@ struct Worker {
     const unsigned lt = (1u << lane) - 1;
     for (int base = 0; base < live; base += 32) {
       int i = base + lane;
-      bool valid = i < live;
-      int32_t t = valid ? xx[i] : 0;
-      bool keep = valid && xx_adjacent(t, v, gv);
+      bool valid_i = i < live;
+      int32_t t = valid_i ? xx[i] : 0;
+      bool keep = valid_i && xx_adjacent(t, v, gv);
       unsigned km = __ballot_sync(FULLMASK, keep);
-      unsigned dm = __ballot_sync(FULLMASK, valid && !keep);
+      unsigned dm = __ballot_sync(FULLMASK, valid_i && !keep);
       if (keep) xx[kept + __popc(km & lt)] = t;
-      else if (valid) xtmp[dropped + __popc(dm & lt)] = t;
+      else if (valid_i) xtmp[dropped + __popc(dm & lt)] = t;
       kept += __popc(km);
       dropped += __popc(dm);
     }
@@ -298,43 +376,57 @@ struct Worker {
     return kept;
   }
 
-  // pivot (bk.py:82-110); returns this lane's word of P - N(pivot)
-  __device__ uint32_t pivot_branches(uint32_t P, uint32_t XP, int live) {
-    if (lane < W) sP[lane] = P;
-    __syncwarp();
-    const uint32_t C = P | XP;
-    const unsigned cmask = __ballot_sync(FULLMASK, C != 0);
-    const unsigned pmask = __ballot_sync(FULLMASK, P != 0);
-    int best = -1, bestc = 0x7fffffff;
-    for (unsigned cm = cmask; cm; cm &= cm - 1) {
-      const int w = __ffs(cm) - 1;
-      const uint32_t Cw = __shfl_sync(FULLMASK, C, w);
-      const int c = w * 32 + lane;
-      int cnt = 0;
-      for (unsigned pm = pmask; pm; pm &= pm - 1) {
-        const int j = __ffs(pm) - 1;
-        cnt += __popc(rowsT[j * CAPP + c] & sP[j]);
+  // number of P members adjacent to candidate column c (lane-private c)
+  __device__ __forceinline__ int count_in_p(const unsigned (&pmask)[K], int c, bool xrow) const {
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      for (unsigned pm = pmask[k]; pm; pm &= pm - 1) {
+        const int j = k * 32 + __ffs(pm) - 1;
+        const uint32_t rw = xrow ? xrowsT[(size_t)j * a.xcap + c] : rowsT[j * CAPP + c];
+        cnt += __popc(rw & sP[j]);
       }
-      if (((Cw >> lane) & 1u) && cnt > best) {
-        best = cnt;
-        bestc = c;
+    }
+    return cnt;
+  }
+
+  // pivot (bk.py:82-110); BR = P - N(pivot)
+  __device__ void pivot_branches(const B& P, const B& XP, int live, B& BR) {
+    unsigned pmask[K], cmask[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (valid(k, lane)) sP[word(k)] = P.w[k];
+      pmask[k] = __ballot_sync(FULLMASK, P.w[k] != 0);
+      cmask[k] = __ballot_sync(FULLMASK, (P.w[k] | XP.w[k]) != 0);
+    }
+    __syncwarp();
+    int best = -1, bestc = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t Ck = P.w[k] | XP.w[k];
+      for (unsigned cm = cmask[k]; cm; cm &= cm - 1) {
+        const int fl = __ffs(cm) - 1;
+        const uint32_t Cw = __shfl_sync(FULLMASK, Ck, fl);
+        const int c = ((k * 32 + fl) << 5) + lane;
+        if ((Cw >> lane) & 1u) {
+          const int cnt = count_in_p(pmask, c, false);
+          if (cnt > best) {
+            best = cnt;
+            bestc = c;
+          }
+        }
       }
     }
     const int m = (int)__reduce_max_sync(FULLMASK, (unsigned)(best + 1)) - 1;
     const int pc = __reduce_min_sync(FULLMASK, best == m ? bestc : 0x7fffffff);
-    uint32_t prow;
+    B prow;
     bool use_local = true;
     if (PIVOT_XX && live > 0) {
       int xb = -1, xpos = 0x7fffffff;
       for (int base = 0; base < live; base += 32) {
         const int i = base + lane;
         if (i < live) {
-          const int32_t t = xx[i];
-          int cnt = 0;
-          for (unsigned pm = pmask; pm; pm &= pm - 1) {
-            const int j = __ffs(pm) - 1;
-            cnt += __popc(xrowsT[(size_t)j * a.xcap + t] & sP[j]);
-          }
+          const int cnt = count_in_p(pmask, xx[i], true);
           if (cnt > xb) {
             xb = cnt;
             xpos = i;
@@ -344,14 +436,14 @@ struct Worker {
       const int xm = (int)__reduce_max_sync(FULLMASK, (unsigned)(xb + 1)) - 1;
       if (xm > m) {
         const int pos = __reduce_min_sync(FULLMASK, xb == xm ? xpos : 0x7fffffff);
-        const int32_t t = xx[pos];
-        prow = (lane < W) ? xrowsT[(size_t)lane * a.xcap + t] : 0u;
+        xrow_of(xx[pos], prow);
         use_local = false;
       }
     }
-    if (use_local) prow = (lane < W) ? row_word(pc, lane) : 0u;
+    if (use_local) row_of(pc, prow);
     __syncwarp();
-    return P & ~prow;
+#pragma unroll
+    for (int k = 0; k < K; ++k) BR.w[k] = P.w[k] & ~prow.w[k];
   }
 
   __device__ void report(int size, uint64_t hs) {
@@ -383,7 +475,7 @@ struct Worker {
   }
 
   // donate the branch (v, childP, childXP) to an idle worker (scheduler.py:417-438)
-  __device__ bool try_donate(uint32_t childP, uint32_t childXP, int v, int32_t gv, int live,
+  __device__ bool try_donate(const B& childP, const B& childXP, int v, int32_t gv, int live,
                              int rlen) {
     int rid = -1;
     const unsigned long long st = *(volatile unsigned long long*)&a.wl->state;
@@ -398,13 +490,13 @@ struct Worker {
         const int src = __ffs(m) - 1;
         m &= m - 1;
         const unsigned wbits = __shfl_sync(FULLMASK, bits, src);
-        const int word = __shfl_sync(FULLMASK, wi, src);
+        const int wordi = __shfl_sync(FULLMASK, wi, src);
         const int b = __ffs(wbits) - 1;
         int claimed = -1;
         if (lane == 0) {
-          const unsigned old = atomicAnd(&a.idle_bits[word], ~(1u << b));
+          const unsigned old = atomicAnd(&a.idle_bits[wordi], ~(1u << b));
           if (old & (1u << b)) {
-            claimed = word * 32 + b;
+            claimed = wordi * 32 + b;
             atomicAdd(&a.wl->state, 1ull);  // one more donation in flight
           }
         }
@@ -414,6 +506,7 @@ struct Worker {
     rid = __shfl_sync(FULLMASK, rid, 0);
     if (rid < 0) return false;
     Mailbox* mb = a.mbox + rid;
+    uint32_t* mbits = a.mbits + (size_t)rid * 2 * W;
     int32_t* rx = a.xx + (size_t)rid * a.xcap;
     int32_t* rr = a.rpath + (size_t)rid * (a.levels + 2);
     // receiver's X_X: the live tokens adjacent to v, in prefix order
@@ -427,6 +520,13 @@ struct Worker {
       k += __popc(km);
     }
     for (int i = lane; i < rlen; i += 32) rr[i] = rpath[i];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      if (valid(q, lane)) {
+        mbits[word(q)] = childP.w[q];
+        mbits[W + word(q)] = childXP.w[q];
+      }
+    }
     if (lane == 0) {
       rr[rlen] = gv;
       mb->origin = origin;
@@ -434,8 +534,6 @@ struct Worker {
       mb->nxx = k;
       mb->has_task = 1;
     }
-    mb->P[lane] = childP;
-    mb->XP[lane] = childXP;
     __threadfence();
     __syncwarp();
     if (lane == 0) atomicExch(&a.wl_wake[rid], 1);
@@ -478,63 +576,87 @@ struct Worker {
   }
 
   // ---------------------------------------------------------------- DFS
+  __device__ __forceinline__ void push(int depth, const B& P, const B& XP, const B& BR) {
+    uint32_t* f = stk + (size_t)depth * 3 * W;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (valid(k, lane)) {
+        f[word(k)] = P.w[k];
+        f[W + word(k)] = XP.w[k];
+        f[2 * W + word(k)] = BR.w[k];
+      }
+    }
+  }
+  __device__ __forceinline__ void pop(int depth, B& P, B& XP, B& BR) const {
+    const uint32_t* f = stk + (size_t)depth * 3 * W;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      P.w[k] = valid(k, lane) ? f[word(k)] : 0u;
+      XP.w[k] = valid(k, lane) ? f[W + word(k)] : 0u;
+      BR.w[k] = valid(k, lane) ? f[2 * W + word(k)] : 0u;
+    }
+  }
+
   // Traverse from the level-0 state (P, XP, xx[0, nxx), rpath[0, rlen)).
-  __device__ void traverse(uint32_t P, uint32_t XP, int nxx, int rlen) {
+  __device__ void traverse(B P, B XP, int nxx, int rlen) {
     uint64_t hs = 0;
     for (int i = 0; i < rlen; ++i) hs += a.vhash[rpath[i]];
-    const bool p_empty = __ballot_sync(FULLMASK, P != 0) == 0;
-    if (p_empty) {  // scheduler.py:300-304
+    if (!any(P)) {  // scheduler.py:300-304
       nodes++;
-      const bool x_empty = __ballot_sync(FULLMASK, XP != 0) == 0 && nxx == 0;
-      if (x_empty) report(rlen, hs);
+      if (!any(XP) && nxx == 0) report(rlen, hs);
       return;
     }
     int depth = 0;
-    int below = 0;  // frozen frames with branches left (scheduler.py:348)
+    int below = 0;  // frozen frames with branches left (scheduler.py:346-348)
     if (lane == 0) {
       lpx[0] = nxx;
       hsum[rlen] = hs;
     }
     int live = nxx;
     nodes++;
-    uint32_t BR = pivot_branches(P, XP, live);
+    B BR;
+    pivot_branches(P, XP, live, BR);
     for (;;) {
-      const unsigned bm = __ballot_sync(FULLMASK, BR != 0);
-      if (bm == 0) {
+      const int v = first(BR);
+      if (v < 0) {
         if (depth == 0) break;
         depth--;
         rlen--;
-        if (lane < W) {
-          const uint32_t* f = stk + (size_t)depth * 3 * W;
-          P = f[lane];
-          XP = f[W + lane];
-          BR = f[2 * W + lane];
-        }
-        if (__ballot_sync(FULLMASK, BR != 0)) below--;
+        pop(depth, P, XP, BR);
+        if (any(BR)) below--;
         live = lpx[depth];
         continue;
       }
-      const int fl = __ffs(bm) - 1;
-      const uint32_t word = __shfl_sync(FULLMASK, BR, fl);
-      const int b = __ffs(word) - 1;
-      const int v = fl * 32 + b;
-      if (lane == fl) {
-        const uint32_t bit = 1u << b;
-        BR &= ~bit;
-        P &= ~bit;
-        XP |= bit;
+      {
+        const int kv = v >> 10, lv = (v >> 5) & 31;
+        const uint32_t bit = 1u << (v & 31);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (k == kv && lane == lv) {
+            BR.w[k] &= ~bit;
+            P.w[k] &= ~bit;
+            XP.w[k] |= bit;
+          }
+        }
       }
-      const uint32_t rowv = (lane < W) ? row_word(v, lane) : 0u;
-      const uint32_t childP = P & rowv;
-      const int cpop = __reduce_add_sync(FULLMASK, __popc(childP));
+      B rowv, childP;
+      row_of(v, rowv);
+#pragma unroll
+      for (int k = 0; k < K; ++k) childP.w[k] = P.w[k] & rowv.w[k];
+      const int cpop = popc(childP);
       const int32_t gv = plist[v];
-      if (a.worker_list_on && cpop >= a.min_p && below > 0 &&
-          __ballot_sync(FULLMASK, BR != 0) != 0 && phase2()) {
-        if (try_donate(childP, XP & rowv, v, gv, live, rlen)) continue;
+      if (a.worker_list_on && cpop >= a.min_p && below > 0 && any(BR) && phase2()) {
+        B cxp;
+#pragma unroll
+        for (int k = 0; k < K; ++k) cxp.w[k] = XP.w[k] & rowv.w[k];
+        if (try_donate(childP, cxp, v, gv, live, rlen)) continue;
       }
       if (cpop == 0) {  // scheduler.py:358-369
         nodes++;
-        bool hit = __ballot_sync(FULLMASK, (XP & rowv) != 0) != 0;
+        uint32_t o = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) o |= XP.w[k] & rowv.w[k];
+        bool hit = __any_sync(FULLMASK, o != 0);
         if (!hit) hit = xx_any_adjacent(v, gv, live);
         if (!hit) {
           if (lane == 0) rpath[rlen] = gv;
@@ -544,17 +666,15 @@ struct Worker {
         continue;
       }
       const int kept = partition(v, gv, live);
-      if (lane < W) {
-        uint32_t* f = stk + (size_t)depth * 3 * W;
-        f[lane] = P;
-        f[W + lane] = XP;
-        f[2 * W + lane] = BR;
-      }
-      if (__ballot_sync(FULLMASK, BR != 0)) below++;
+      push(depth, P, XP, BR);
+      if (any(BR)) below++;
       depth++;
       live = kept;
-      XP &= rowv;
-      P = childP;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        XP.w[k] &= rowv.w[k];
+        P.w[k] = childP.w[k];
+      }
       if (lane == 0) {
         lpx[depth] = kept;
         rpath[rlen] = gv;
@@ -563,30 +683,41 @@ struct Worker {
       rlen++;
       nodes++;
       __syncwarp();
-      BR = pivot_branches(P, XP, live);
+      pivot_branches(P, XP, live, BR);
     }
   }
 
   __device__ void run_root(int64_t r) {
     const int nr = build(r);
-    uint32_t P = 0;
-    if (lane < W) {
-      const int lo = lane * 32;
-      if (np >= lo + 32) P = 0xffffffffu;
-      else if (np > lo) P = (1u << (np - lo)) - 1u;
+    B P, XP;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      uint32_t x = 0;
+      if (valid(k, lane)) {
+        const int lo = word(k) * 32;
+        if (np >= lo + 32) x = 0xffffffffu;
+        else if (np > lo) x = (1u << (np - lo)) - 1u;
+      }
+      P.w[k] = x;
+      XP.w[k] = 0u;
     }
     for (int t = lane; t < nx; t += 32) xx[t] = t;
     __syncwarp();
-    traverse(P, 0u, nx, nr);
+    traverse(P, XP, nx, nr);
   }
 
   __device__ void run_donated() {
     const Mailbox* mb = a.mbox + wid;
+    const uint32_t* mbits = a.mbits + (size_t)wid * 2 * W;
     const int64_t r = mb->origin;
     const int rlen = mb->rlen;
     const int nxx = mb->nxx;
-    const uint32_t P = (lane < W) ? mb->P[lane] : 0u;
-    const uint32_t XP = (lane < W) ? mb->XP[lane] : 0u;
+    B P, XP;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      P.w[k] = valid(k, lane) ? mbits[word(k)] : 0u;
+      XP.w[k] = valid(k, lane) ? mbits[W + word(k)] : 0u;
+    }
     // rebuild the origin's induced rows; rpath/xx were written by the donor,
     // so save the donated path across build()'s R0 write
     int32_t keep0 = 0, keep1 = 0;
@@ -608,10 +739,11 @@ template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
+  constexpr int SPW = W < 32 ? 32 : W;  // sP words per warp
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem);
   uint32_t* s_p = reinterpret_cast<uint32_t*>(s_hist + HIST_SMEM);
-  uint32_t* s_rows = s_p + WARPS * 32;
+  uint32_t* s_rows = s_p + WARPS * SPW;
   int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? WARPS * W * CAPP : 0));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -620,9 +752,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
   const int wid = blockIdx.x * WARPS + warp;
   if (wid < a.num_workers) {
     Worker<W, PIVOT_XX, XROWS, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
-                                  s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + warp * 32,
+                                  s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + warp * SPW,
                                   s_hist);
-    for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-260)
+    for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-273)
       unsigned long long idx = 0;
       if (lane == 0) idx = atomicAdd(a.root_counter, 1ull);
       idx = __shfl_sync(FULLMASK, idx, 0);
@@ -659,13 +791,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
 // Root keys: class (bitset width) in the top byte, then heaviest-first by an
 // estimated subtree cost.  l1 roots: |P| = |N+(v)|, |X| = |N-(v)|; l2 roots
 // (edges u < v): bounded by |N+(v)| and |N-(v)|.
+constexpr int NUM_WIDTHS = 8;
+constexpr int TRIVIAL_RANK = NUM_WIDTHS;       // first-level roots with P empty
+constexpr int MAXP_SLOT = NUM_WIDTHS + 1;      // classes[] slot holding max |P|
+constexpr int MAX_CAPACITY_BITS = 32 * 128;    // widest instantiated bitset
 __device__ __forceinline__ int width_rank(int64_t p) {
-  if (p > 512) return 0;   // W = 32
-  if (p > 256) return 1;   // 16
-  if (p > 128) return 2;   // 8
-  if (p > 64) return 3;    // 4
-  if (p > 32) return 4;    // 2
-  return 5;                // 1
+  if (p > 2048) return 0;  // W = 128
+  if (p > 1024) return 1;  // 64
+  if (p > 512) return 2;   // 32
+  if (p > 256) return 3;   // 16
+  if (p > 128) return 4;   // 8
+  if (p > 64) return 5;    // 4
+  if (p > 32) return 6;    // 2
+  return 7;                // 1
 }
 
 __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
@@ -674,8 +812,8 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
                             int64_t count, uint64_t* __restrict__ keys,
                             int64_t* __restrict__ roots, unsigned long long* __restrict__ classes,
                             unsigned long long* __restrict__ max_p) {
-  __shared__ unsigned long long s_cls[8];
-  if (threadIdx.x < 8) s_cls[threadIdx.x] = 0;
+  __shared__ unsigned long long s_cls[TRIVIAL_RANK + 1];
+  if (threadIdx.x <= TRIVIAL_RANK) s_cls[threadIdx.x] = 0;
   __syncthreads();
   unsigned long long local_max = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
@@ -698,7 +836,7 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
       x = split[v] - ro[v];
       roots[i] = (u << 32) | v;
     }
-    const int rank = (roots_mode == 1 && p == 0) ? 6 : width_rank(p);
+    const int rank = (roots_mode == 1 && p == 0) ? TRIVIAL_RANK : width_rank(p);
     uint64_t cost = (uint64_t)(p + 1) * (uint64_t)(p + 1) + (uint64_t)(p + 1) * (uint64_t)x / 8;
     const uint64_t lim = (1ull << 56) - 1;
     if (cost > lim) cost = lim;
@@ -707,7 +845,8 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
     if ((unsigned long long)p > local_max) local_max = p;
   }
   __syncthreads();
-  if (threadIdx.x < 7 && s_cls[threadIdx.x]) atomicAdd(&classes[threadIdx.x], s_cls[threadIdx.x]);
+  if (threadIdx.x <= TRIVIAL_RANK && s_cls[threadIdx.x])
+    atomicAdd(&classes[threadIdx.x], s_cls[threadIdx.x]);
   if (local_max) atomicMax(max_p, local_max);
 }
 
@@ -827,7 +966,8 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
   auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
-  size_t smem = HIST_SMEM * sizeof(unsigned long long) + WARPS * 32 * sizeof(uint32_t) +
+  constexpr int SPW = W < 32 ? 32 : W;
+  size_t smem = HIST_SMEM * sizeof(unsigned long long) + WARPS * SPW * sizeof(uint32_t) +
                 (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
   MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0, per_sm = 0;
@@ -840,11 +980,13 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   }
   // every worker must be co-resident: idle workers spin until woken
   int64_t resident = (int64_t)per_sm * sms * WARPS;
-  const int64_t levels = CAP + 3;
+  // DFS depth <= |P| of the root: the class's stack never exceeds min(CAP, max |P|)
+  const int64_t levels = std::min<int64_t>(CAP, std::max<int64_t>(args.levels, 1)) + 3;
   const int64_t xcap = std::max<int64_t>(args.xcap, 1);
   size_t per_worker = sizeof(uint32_t) * (size_t)(levels * 3 * W) + sizeof(int32_t) * levels +
                       (sizeof(int32_t) + sizeof(uint64_t)) * (levels + 2) +
-                      sizeof(int32_t) * 2 * xcap + sizeof(Mailbox) + sizeof(int) * 2 +
+                      sizeof(int32_t) * 2 * xcap + sizeof(Mailbox) + sizeof(uint32_t) * 2 * W +
+                      sizeof(int) * 2 +
                       sizeof(long long) * 4 +
                       (XROWS ? sizeof(uint32_t) * (size_t)W * xcap : 0) +
                       (args.roots_mode == 2 ? sizeof(int32_t) * xcap : 0) +
@@ -868,7 +1010,8 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   if (get(&args.stack, (size_t)workers * levels * 3 * W) || get(&args.lpx, (size_t)workers * levels) ||
       get(&args.rpath, (size_t)workers * (levels + 2)) || get(&args.hsum, (size_t)workers * (levels + 2)) ||
       get(&args.xx, (size_t)workers * xcap) || get(&args.xtmp, (size_t)workers * xcap) ||
-      get(&args.mbox, (size_t)workers) || get(&args.idle_bits, (size_t)(workers + 31) / 32) ||
+      get(&args.mbox, (size_t)workers) || get(&args.mbits, (size_t)workers * 2 * W) ||
+      get(&args.idle_bits, (size_t)(workers + 31) / 32) ||
       get(&args.wl_wake, (size_t)workers) || get(&args.wl, 1) ||
       get(&args.root_counter, 1))
     return -1;
@@ -908,6 +1051,8 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
     case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget, ev, xr);
     case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget, ev, xr);
     case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
+    case 64: return launch_class<64, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
+    case 128: return launch_class<128, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
   }
   mce_set_error("unsupported bitset width %d", W);
   return -3;
@@ -1007,13 +1152,13 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     int64_t *roots = nullptr, *roots2 = nullptr;
     unsigned long long* cls = nullptr;
     if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count) ||
-        get(&cls, 8)) {
+        get(&cls, MAXP_SLOT + 1)) {
       cleanup();
       return -1;
     }
-    MCE_CHECK(cudaMemsetAsync(cls, 0, 8 * sizeof(unsigned long long), s));
+    MCE_CHECK(cudaMemsetAsync(cls, 0, (MAXP_SLOT + 1) * sizeof(unsigned long long), s));
     k_root_keys<<<grid_for(count), 256, 0, s>>>(g->ro, g->split, g->col, eoff, n, cfg->roots,
-                                                 begin, stride, count, keys, roots, cls, cls + 7);
+                                                 begin, stride, count, keys, roots, cls, cls + MAXP_SLOT);
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(keys, keys2);
@@ -1024,21 +1169,23 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
     MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 64, s));
     cudaFreeAsync(tmp, s);
-    unsigned long long hc[8];
+    unsigned long long hc[MAXP_SLOT + 1];
     MCE_CHECK(cudaMemcpyAsync(hc, cls, sizeof(hc), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
     const int64_t* sorted_roots = dv.Current();
-    const int64_t cap_limit = std::min<int64_t>(cfg->capacity_bits > 0 ? cfg->capacity_bits : 1024, 1024);
-    if ((int64_t)hc[7] > cap_limit) {
-      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld", (long long)hc[7],
+    const int64_t cap_limit = std::min<int64_t>(
+        cfg->capacity_bits > 0 ? cfg->capacity_bits : MAX_CAPACITY_BITS, MAX_CAPACITY_BITS);
+    const int64_t max_p = (int64_t)hc[MAXP_SLOT];
+    if (max_p > cap_limit) {
+      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld", (long long)max_p,
                     (long long)cap_limit);
       cleanup();
       return -4;
     }
-    const int widths[6] = {32, 16, 8, 4, 2, 1};
+    const int widths[NUM_WIDTHS] = {128, 64, 32, 16, 8, 4, 2, 1};
     std::vector<ClassPlan> plan;
     int64_t i = 0;
-    for (int c = 0; c < 6; ++c) {
+    for (int c = 0; c < NUM_WIDTHS; ++c) {
       if (hc[c]) plan.push_back({widths[c], i, (int64_t)hc[c]});
       i += (int64_t)hc[c];
     }
@@ -1073,6 +1220,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.num_roots = cp.count;
       args.roots_mode = cfg->roots;
       args.xcap = g->max_earlier;
+      args.levels = (int)max_p;
       args.g_acc = acc;
       args.g_hist = hist;
       args.w_metrics = wmet;

@@ -70,14 +70,19 @@ int bits_for(int64_t n) {
 
 // ---------------------------------------------------------------- kernels
 
-__global__ void k_edge_keys(const int64_t* __restrict__ edges, int64_t m, int b,
-                            uint64_t* __restrict__ keys) {
+// (lo << b | hi) keys; self-loops become ~0 (dropped); ids outside [0, n)
+// raise `bad` (reference: ValueError, graph.py:103-129)
+__global__ void k_edge_keys(const int64_t* __restrict__ edges, int64_t m, int b, int64_t n,
+                            uint64_t* __restrict__ keys, int* __restrict__ bad) {
+  bool oob = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t a = edges[2 * i], c = edges[2 * i + 1];
+    const int64_t a = edges[2 * i], c = edges[2 * i + 1];
+    oob |= (a < 0) | (c < 0) | (a >= n) | (c >= n);
     int64_t lo = a < c ? a : c, hi = a < c ? c : a;
     keys[i] = (lo == hi) ? ~0ull : (((uint64_t)lo << b) | (uint64_t)hi);
   }
+  if (__syncthreads_or(oob) && threadIdx.x == 0) atomicExch(bad, 1);
 }
 
 struct NotAllOnes {
@@ -161,57 +166,172 @@ __global__ void k_split(const int64_t* __restrict__ ro, const int32_t* __restric
 
 // ---- parallel peel
 
-__global__ void k_init_peel(const int64_t* __restrict__ ro, int64_t n, int32_t* __restrict__ deg,
-                            int32_t* __restrict__ alive, uint8_t* __restrict__ removed) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+// ---- persistent parallel peel: the whole bucket-peeling loop in ONE
+// cooperative launch (no host round trip per round).  Round structure:
+//   1. each CTA scans its contiguous chunk of the alive list: how many have
+//      deg <= k ("take"), and the minimum alive degree;     grid sync
+//   2. every CTA reduces the per-CTA counts identically (so all CTAs take the
+//      same branch): nf == 0 -> k = max(k+1, min deg), next round;
+//      else rank the takes (base + exclusive prefix, alive-list = id order)
+//      and compact the keeps into the other alive buffer;   grid sync
+//   3. warps decrement the live neighbours of the frontier;  grid sync
+// Per-CTA counters are double-buffered by round parity: a CTA can run at
+// most one round ahead of the slowest (a grid sync separates them).
+constexpr int PEEL_THREADS = 512;
+
+struct PeelCounters {
+  int64_t take[2];
+  int32_t mindeg[2];
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsigned int* gen,
+                                             unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd((unsigned int*)gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(PEEL_THREADS)
+k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+                  int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
+                  int32_t* __restrict__ frontier, uint8_t* __restrict__ removed,
+                  int64_t* __restrict__ pos, PeelCounters* __restrict__ blk,
+                  unsigned int* bar, int64_t* __restrict__ out_degeneracy) {
+  typedef cub::BlockReduce<int64_t, PEEL_THREADS> BRs;
+  typedef cub::BlockReduce<int32_t, PEEL_THREADS> BRm;
+  typedef cub::BlockScan<int32_t, PEEL_THREADS> BS;
+  __shared__ union {
+    typename BRs::TempStorage rs;
+    typename BRm::TempStorage rm;
+    typename BS::TempStorage sc;
+  } tmp;
+  __shared__ int64_t s_nf, s_prefix;
+  __shared__ int32_t s_min;
+  const unsigned int G = gridDim.x;
+  const int tid = threadIdx.x;
+  unsigned int* bar_count = bar;
+  volatile unsigned int* bar_gen = bar + 1;
+
+  for (int64_t v = blockIdx.x * (int64_t)PEEL_THREADS + tid; v < n; v += (int64_t)G * PEEL_THREADS) {
     deg[v] = (int32_t)(ro[v + 1] - ro[v]);
-    alive[v] = (int32_t)v;
+    alive_a[v] = (int32_t)v;
     removed[v] = 0;
   }
-}
+  grid_barrier(bar_count, bar_gen, G);
 
-__global__ void k_peel_flags(const int32_t* __restrict__ alive, int64_t na,
-                             const int32_t* __restrict__ deg, int32_t k,
-                             uint8_t* __restrict__ take, uint8_t* __restrict__ keep) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    bool t = deg[alive[i]] <= k;
-    take[i] = t;
-    keep[i] = !t;
-  }
-}
-
-__global__ void k_peel_assign(const int32_t* __restrict__ frontier, int64_t nf, int64_t base,
-                              int64_t* __restrict__ position, uint8_t* __restrict__ removed) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t v = frontier[i];
-    position[v] = base + i;
-    removed[v] = 1;
-  }
-}
-
-// one warp per frontier vertex: decrement the live neighbours' degrees
-__global__ void k_peel_decrement(const int32_t* __restrict__ frontier, int64_t nf,
-                                 const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                                 const uint8_t* __restrict__ removed, int32_t* __restrict__ deg) {
-  const int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < nf; i += nwarps) {
-    int32_t v = frontier[i];
-    for (int64_t e = ro[v] + lane; e < ro[v + 1]; e += 32) {
-      int32_t u = col[e];
-      if (!removed[u]) atomicSub(&deg[u], 1);
+  int32_t* alive = alive_a;
+  int32_t* alive2 = alive_b;
+  int64_t na = n, base = 0;
+  int32_t k = 0, deg_max = 0;
+  int parity = 0;
+  while (na > 0) {
+    const int64_t chunk = (na + G - 1) / G;
+    const int64_t c0 = min((int64_t)blockIdx.x * chunk, na);
+    const int64_t c1 = min(c0 + chunk, na);
+    // 1. count takes and the minimum alive degree of this CTA's chunk
+    int64_t t = 0;
+    int32_t mn = 0x7fffffff;
+    for (int64_t i = c0 + tid; i < c1; i += PEEL_THREADS) {
+      const int32_t d = __ldcg(&deg[__ldcg(&alive[i])]);
+      t += (d <= k);
+      mn = min(mn, d);
     }
+    t = BRs(tmp.rs).Sum(t);
+    __syncthreads();
+    mn = BRm(tmp.rm).Reduce(mn, cub::Min());
+    if (tid == 0) {
+      blk[blockIdx.x].take[parity] = t;
+      blk[blockIdx.x].mindeg[parity] = mn;
+    }
+    grid_barrier(bar_count, bar_gen, G);
+    // 2. identical reduction in every CTA
+    int64_t tot = 0, pre = 0;
+    int32_t gmin = 0x7fffffff;
+    for (unsigned int b = tid; b < G; b += PEEL_THREADS) {
+      const int64_t tb = __ldcg(&blk[b].take[parity]);
+      tot += tb;
+      if (b < blockIdx.x) pre += tb;
+      gmin = min(gmin, __ldcg(&blk[b].mindeg[parity]));
+    }
+    __syncthreads();
+    tot = BRs(tmp.rs).Sum(tot);
+    __syncthreads();
+    if (tid == 0) s_nf = tot;
+    __syncthreads();
+    pre = BRs(tmp.rs).Sum(pre);
+    __syncthreads();
+    gmin = BRm(tmp.rm).Reduce(gmin, cub::Min());
+    if (tid == 0) {
+      s_prefix = pre;
+      s_min = gmin;
+    }
+    __syncthreads();
+    const int64_t nf = s_nf;
+    parity ^= 1;
+    if (nf == 0) {
+      k = max(k + 1, s_min);
+      continue;
+    }
+    if (k > deg_max) deg_max = k;
+    // rank the takes in alive order, compact the keeps
+    int64_t run_take = s_prefix;            // takes before this tile, grid-wide
+    for (int64_t tile = c0; tile < c1; tile += PEEL_THREADS) {
+      const int64_t i = tile + tid;
+      int32_t v = 0, flag = 0;
+      if (i < c1) {
+        v = __ldcg(&alive[i]);
+        flag = __ldcg(&deg[v]) <= k;
+      }
+      int32_t excl = 0, tile_total = 0;
+      BS(tmp.sc).ExclusiveSum(flag, excl, tile_total);
+      __syncthreads();
+      if (i < c1) {
+        if (flag) {
+          const int64_t r = run_take + excl;
+          pos[v] = base + r;
+          frontier[r] = v;
+          removed[v] = 1;
+        } else {
+          alive2[i - run_take - excl] = v;  // keeps before i, grid-wide
+        }
+      }
+      run_take += tile_total;
+    }
+    grid_barrier(bar_count, bar_gen, G);
+    // 3. decrement live neighbours of the frontier (one warp per vertex)
+    {
+      const int lane = tid & 31;
+      const int64_t warp = ((int64_t)blockIdx.x * PEEL_THREADS + tid) >> 5;
+      const int64_t nwarps = ((int64_t)G * PEEL_THREADS) >> 5;
+      for (int64_t f = warp; f < nf; f += nwarps) {
+        const int32_t v = __ldcg(&frontier[f]);
+        const int64_t e1 = ro[v + 1];
+        for (int64_t e = ro[v] + lane; e < e1; e += 32) {
+          const int32_t u = col[e];
+          if (!__ldcg(&removed[u])) atomicSub(&deg[u], 1);
+        }
+      }
+    }
+    grid_barrier(bar_count, bar_gen, G);
+    int32_t* t2 = alive;
+    alive = alive2;
+    alive2 = t2;
+    base += nf;
+    na -= nf;
   }
+  if (blockIdx.x == 0 && tid == 0) *out_degeneracy = deg_max;
 }
-
-struct DegOf {
-  const int32_t* deg;
-  __host__ __device__ int32_t operator()(const int32_t& v) const { return deg[v]; }
-};
 
 // ---- exact order (reference tie-break): single CTA, min-segment-tree over
 // keys (deg << 32 | id).  Sequential by nature; used for reference-identical
@@ -337,6 +457,41 @@ int csr_from_sorted_keys(mce_graph* g, uint64_t* keys, int64_t nnz, int b, cudaS
   return mce_graph_build_split(g, s);
 }
 
+// Bucket peeling in one persistent launch; positions to d_pos (device).
+int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaStream_t s) {
+  const int64_t n = g->n;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_persistent,
+                                                          PEEL_THREADS, 0));
+  if (per_sm < 1) {
+    mce_set_error("peel kernel does not fit on an SM");
+    return -3;
+  }
+  // every CTA must be co-resident (software grid barrier)
+  int64_t grid = std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, (n + 4095) / 4096));
+  int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *frontier = nullptr;
+  uint8_t* removed = nullptr;
+  PeelCounters* blk = nullptr;
+  unsigned int* bar = nullptr;
+  int64_t* d_deg = nullptr;
+  if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
+      dev_alloc(&frontier, n, s) || dev_alloc(&removed, n, s) || dev_alloc(&blk, grid, s) ||
+      dev_alloc(&bar, 2, s) || dev_alloc(&d_deg, 1, s))
+    return -1;
+  MCE_CHECK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s));
+  k_peel_persistent<<<(int)grid, PEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2,
+                                                      frontier, removed, d_pos, blk, bar, d_deg);
+  mce_count_launch();
+  MCE_CHECK(cudaGetLastError());
+  MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaStreamSynchronize(s));
+  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(frontier, s);
+  dev_free(removed, s); dev_free(blk, s); dev_free(bar, s); dev_free(d_deg, s);
+  return 0;
+}
+
 }  // namespace
 
 int mce_graph_build_split(mce_graph* g, cudaStream_t s) {
@@ -384,25 +539,34 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
   int64_t m = 0;
   if (num_edges > 0) {
     uint64_t* raw = nullptr;
-    if (dev_alloc(&raw, num_edges, s)) return -1;
-    k_edge_keys<<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, raw);
+    int64_t* d_cnt = nullptr;  // [0] selected count, [1] out-of-range flag
+    if (dev_alloc(&raw, num_edges, s) || dev_alloc(&d_cnt, 2, s)) return -1;
+    MCE_CHECK(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(int64_t), s));
+    k_edge_keys<<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, num_vertices, raw,
+                                                    (int*)(d_cnt + 1));
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     dev_free(owned, s);
     // drop self-loops
     if (dev_alloc(&keys, num_edges, s)) return -1;
-    int64_t* d_cnt = nullptr;
-    if (dev_alloc(&d_cnt, 1, s)) return -1;
     size_t tb = 0;
     MCE_CHECK(cub::DeviceSelect::If(nullptr, tb, raw, keys, d_cnt, num_edges, NotAllOnes(), s));
     void* tmp = nullptr;
     MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
     MCE_CHECK(cub::DeviceSelect::If(tmp, tb, raw, keys, d_cnt, num_edges, NotAllOnes(), s));
     cudaFreeAsync(tmp, s);
-    int64_t kept = 0;
-    MCE_CHECK(cudaMemcpyAsync(&kept, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    int64_t hk[2] = {0, 0};
+    MCE_CHECK(cudaMemcpyAsync(hk, d_cnt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
     dev_free(raw, s);
+    const int64_t kept = hk[0];
+    if (hk[1]) {
+      dev_free(keys, s);
+      dev_free(d_cnt, s);
+      delete g;
+      mce_set_error("vertex id outside [0, num_vertices)");
+      return -2;
+    }
     if (sort_keys(&keys, kept, 2 * b, s)) return -1;
     // merge duplicates
     uint64_t* uniq = nullptr;
@@ -542,65 +706,8 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
     dev_free(tree, s);
     dev_free(d_deg, s);
   } else {
-    int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *frontier = nullptr;
-    uint8_t *removed = nullptr, *take = nullptr, *keep = nullptr;
-    int64_t* d_cnt = nullptr;
-    int32_t* d_min = nullptr;
-    if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
-        dev_alloc(&frontier, n, s) || dev_alloc(&removed, n, s) || dev_alloc(&take, n, s) ||
-        dev_alloc(&keep, n, s) || dev_alloc(&d_cnt, 2, s) || dev_alloc(&d_min, 1, s))
-      return -1;
-    k_init_peel<<<grid_for(n), 256, 0, s>>>(g->ro, n, deg, alive, removed);
-    mce_count_launch();
-    MCE_CHECK(cudaGetLastError());
-    size_t tb_sel = 0, tb_min = 0;
-    MCE_CHECK(cub::DeviceSelect::Flagged(nullptr, tb_sel, alive, take, frontier, d_cnt, n, s));
-    cub::TransformInputIterator<int32_t, DegOf, const int32_t*> degs(alive, DegOf{deg});
-    MCE_CHECK(cub::DeviceReduce::Min(nullptr, tb_min, degs, d_min, n, s));
-    void* tmp = nullptr;
-    size_t tb = std::max(tb_sel, tb_min);
-    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
-    int64_t na = n, base = 0;
-    int32_t k = 0;
-    int64_t deg_max = 0;
-    while (na > 0) {
-      k_peel_flags<<<grid_for(na), 256, 0, s>>>(alive, na, deg, k, take, keep);
-      mce_count_launch();
-      size_t t1 = tb;
-      MCE_CHECK(cub::DeviceSelect::Flagged(tmp, t1, alive, take, frontier, d_cnt, na, s));
-      int64_t nf = 0;
-      MCE_CHECK(cudaMemcpyAsync(&nf, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      MCE_CHECK(cudaStreamSynchronize(s));
-      if (nf == 0) {
-        cub::TransformInputIterator<int32_t, DegOf, const int32_t*> dg(alive, DegOf{deg});
-        size_t t2 = tb;
-        MCE_CHECK(cub::DeviceReduce::Min(tmp, t2, dg, d_min, na, s));
-        int32_t mn = 0;
-        MCE_CHECK(cudaMemcpyAsync(&mn, d_min, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        MCE_CHECK(cudaStreamSynchronize(s));
-        k = std::max(k + 1, mn);
-        continue;
-      }
-      if (k > deg_max) deg_max = k;
-      k_peel_assign<<<grid_for(nf), 256, 0, s>>>(frontier, nf, base, d_pos, removed);
-      mce_count_launch();
-      k_peel_decrement<<<grid_for(nf * 32), 256, 0, s>>>(frontier, nf, g->ro, g->col, removed, deg);
-      mce_count_launch();
-      size_t t3 = tb;
-      MCE_CHECK(cub::DeviceSelect::Flagged(tmp, t3, alive, keep, alive2, d_cnt + 1, na, s));
-      MCE_CHECK(cudaGetLastError());
-      std::swap(alive, alive2);
-      base += nf;
-      na -= nf;
-    }
-    // the degeneracy is the largest peel level at which a vertex left, but a
-    // level may be reached only because k jumped to the minimum degree: the
-    // real degree at removal is what the reference reports (graph.py:198-205)
-    *degeneracy = deg_max;
-    cudaFreeAsync(tmp, s);
-    dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(frontier, s);
-    dev_free(removed, s); dev_free(take, s); dev_free(keep, s); dev_free(d_cnt, s);
-    dev_free(d_min, s);
+    int rc = peel_parallel(g, d_pos, degeneracy, s);
+    if (rc) return rc;
   }
   if (!position_on_device) {
     MCE_CHECK(cudaMemcpyAsync(position, d_pos, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
@@ -647,4 +754,21 @@ int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_dev
   return 0;
 }
 
+// Order + relabel without leaving the device (graph.py:239-243 minus stats):
+// positions stay in HBM; the result's labels give the permutation back.
+int mce_preprocess(const mce_graph* g, int method, int64_t* degeneracy, void* stream,
+                   mce_graph** out) {
+  mce_prepare_device();
+  cudaStream_t s = (cudaStream_t)stream;
+  *out = nullptr;
+  *degeneracy = 0;
+  int64_t* d_pos = nullptr;
+  if (dev_alloc(&d_pos, g->n, s)) return -1;
+  int rc = mce_degeneracy_order(g, method, d_pos, 1, degeneracy, stream);
+  if (!rc) rc = mce_reorder(g, d_pos, 1, stream, out);
+  dev_free(d_pos, s);
+  return rc;
+}
+
 }  // extern "C"
+

@@ -78,13 +78,15 @@ class Graph:
 
     def __init__(self, num_vertices: int, row_offsets: np.ndarray | None = None,
                  col_indices: np.ndarray | None = None, edge_list: np.ndarray | None = None,
-                 *, _device: _DeviceGraph | None = None, _labels: np.ndarray | None = None):
+                 *, _device: _DeviceGraph | None = None, _labels: np.ndarray | None = None,
+                 _device_labels: bool = False):
         self.num_vertices = int(num_vertices)
         self._ro = None if row_offsets is None else np.asarray(row_offsets, dtype=np.int64)
         self._ci = None if col_indices is None else np.asarray(col_indices, dtype=np.int64)
         self.edge_list = edge_list
         self._dev = _device
         self._labels = _labels
+        self._device_labels = _device_labels
         self._info: dict | None = None
         if self._dev is None and (self._ro is None or self._ci is None):
             raise ValueError("Graph needs CSR arrays or a device graph")
@@ -130,7 +132,13 @@ class Graph:
 
     @property
     def labels(self) -> np.ndarray | None:
-        """Original label of every vertex (reordered graphs), else None."""
+        """Original label of every vertex (reordered graphs), else None.
+        Copied from the device on first access when the relabel ran there."""
+        if self._labels is None and self._device_labels:
+            lab = np.empty(self.num_vertices, dtype=np.int64)
+            _lib.check(_lib.lib().mce_graph_copy_csr(self._dev.handle, None, None, _lib.ptr(lab),
+                                                     None), "mce_graph_copy_csr")
+            self._labels = lab
         return self._labels
 
     # --- reference accessors ---------------------------------------------
@@ -196,12 +204,31 @@ class GraphStats:
     degeneracy: int
 
 
-@dataclass(frozen=True)
 class DegeneracyOrder:
-    """Permutation original id -> rank plus the degeneracy it realises."""
+    """Permutation original id -> rank plus the degeneracy it realises
+    (reference graph.py:96-100).  ``position`` may be produced lazily (by
+    ``preprocess``, which keeps the permutation on the device)."""
 
-    position: np.ndarray
-    degeneracy: int
+    __slots__ = ("_position", "degeneracy", "_thunk")
+
+    def __init__(self, position: np.ndarray | None, degeneracy: int, _thunk=None) -> None:
+        self._position = position
+        self.degeneracy = int(degeneracy)
+        self._thunk = _thunk
+
+    @property
+    def position(self) -> np.ndarray:
+        if self._position is None:
+            self._position = self._thunk()
+            self._thunk = None
+        return self._position
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, DegeneracyOrder) and self.degeneracy == other.degeneracy
+                and np.array_equal(self.position, other.position))
+
+    def __repr__(self) -> str:
+        return f"DegeneracyOrder(n={len(self.position)}, degeneracy={self.degeneracy})"
 
 
 def _from_device(n: int, h: ctypes.c_void_p, labels: np.ndarray | None = None) -> Graph:
@@ -215,9 +242,7 @@ def from_edges(edges: Iterable[tuple[int, int]] | np.ndarray, num_vertices: int)
     arr = np.ascontiguousarray(
         np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges,
                    dtype=np.int64).reshape(-1, 2))
-    if arr.size and (arr.min() < 0 or arr.max() >= num_vertices):
-        raise ValueError("vertex id outside [0, num_vertices)")
-    h = ctypes.c_void_p()
+    h = ctypes.c_void_p()  # ids outside [0, n) are rejected on the device (ValueError)
     _lib.check(_lib.lib().mce_graph_from_edges(_lib.ptr(arr), len(arr), int(num_vertices), 0,
                                                None, ctypes.byref(h)), "mce_graph_from_edges")
     return _from_device(num_vertices, h)
@@ -319,7 +344,30 @@ def stats(g: Graph, order: DegeneracyOrder) -> GraphStats:
 
 
 def preprocess(g: Graph, method: str = "parallel") -> tuple[Graph, DegeneracyOrder, GraphStats]:
-    """Order, relabel and summarise in one step (reference graph.py:239-243)."""
-    order = degeneracy_order(g, method=method)
-    g2 = reorder(g, order)
+    """Order, relabel and summarise in one step (reference graph.py:239-243).
+
+    One device call (``mce_preprocess``): the permutation never leaves HBM;
+    ``order.position`` is rebuilt from the reordered graph's labels only if
+    host code reads it."""
+    if method not in ORDER_METHODS:
+        raise ValueError(f"unknown ordering method {method!r}")
+    n = g.num_vertices
+    if n == 0:
+        order = DegeneracyOrder(np.empty(0, dtype=np.int64), 0)
+        g2 = from_edges(np.empty((0, 2), dtype=np.int64), 0)
+        return g2, order, stats(g2, order)
+    d = ctypes.c_int64(0)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().mce_preprocess(g.device.handle, ORDER_METHODS[method], ctypes.byref(d),
+                                         None, ctypes.byref(h)), "mce_preprocess")
+    g2 = Graph(n, _device=_DeviceGraph(h), _device_labels=True)
+    base = g.labels
+
+    def position() -> np.ndarray:
+        # labels2[rank] = label(v)  =>  position[v] = rank of label(v)
+        inv = np.empty(n, dtype=np.int64)
+        inv[g2.labels] = np.arange(n, dtype=np.int64)
+        return inv if base is None else inv[base]
+
+    order = DegeneracyOrder(None, int(d.value), _thunk=position)
     return g2, order, stats(g2, order)

@@ -102,7 +102,7 @@ class RunResult:
     total_time: float
     phase1_time: float
     phase2_time: float
-    worker_metrics: list[WorkerMetrics]
+    worker_metrics_raw: np.ndarray | list = field(repr=False)
     nodes_total: int = 0
     clique_hash: int = 0
     size_histogram: dict[int, int] = field(default_factory=dict)
@@ -110,6 +110,21 @@ class RunResult:
     kernel_launches: int = 0
     kernel_ms: float = 0.0
     build_bytes: int = 0
+    timing: bool = False
+
+    @property
+    def worker_metrics(self) -> list[WorkerMetrics]:
+        """Per-worker counters (built on first access from the device's
+        ``[nodes, roots, donations made, received]`` rows)."""
+        raw = self.worker_metrics_raw
+        if isinstance(raw, np.ndarray):
+            out = []
+            for i, row in enumerate(raw.tolist()):
+                m = WorkerMetrics(worker_id=i, enabled=self.timing)
+                m.nodes_visited, m.roots_claimed, m.donations_made, m.donations_received = row
+                out.append(m)
+            self.worker_metrics_raw = raw = out
+        return raw
 
     def report(self):
         from paper_2212_01473_b200.metrics import aggregate
@@ -153,7 +168,7 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
     limit = sink.collect_limit
     if g.num_vertices == 0:
         return RunResult(0, 0, cfg.roots, induced, cfg.resolved_workers(), 0.0, 0.0, 0.0,
-                         [WorkerMetrics(worker_id=0, enabled=cfg.timing)])
+                         [WorkerMetrics(worker_id=0, enabled=cfg.timing)], timing=cfg.timing)
     _lib.require_device()
     cap_words = 0
     if limit:
@@ -195,13 +210,8 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
             sink.collected.extend(got[:room])
     sink.total += int(res.cliques)
     workers = max(int(res.workers), 1)
-    metrics = []
-    for i in range(workers):
-        m = WorkerMetrics(worker_id=i, enabled=cfg.timing)
-        m.nodes_visited, m.roots_claimed, m.donations_made, m.donations_received = (
-            int(x) for x in wm[i])
-        metrics.append(m)
-    hist = {s: int(res.hist[s]) for s in range(_lib.HIST_MAX) if res.hist[s]}
+    hist_arr = np.ctypeslib.as_array(res.hist)
+    hist = {int(s): int(hist_arr[s]) for s in np.flatnonzero(hist_arr)}
     return RunResult(
         clique_count=int(res.cliques),
         donation_count=int(res.donations),
@@ -211,7 +221,7 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
         total_time=t1 - t0,
         phase1_time=t1 - t0,
         phase2_time=0.0,
-        worker_metrics=metrics,
+        worker_metrics_raw=wm[:workers],
         nodes_total=int(res.nodes),
         clique_hash=int(res.hash),
         size_histogram=hist,
@@ -219,4 +229,5 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
         kernel_launches=int(res.launches),
         kernel_ms=float(res.kernel_ms),
         build_bytes=int(res.build_bytes),
+        timing=cfg.timing,
     )

@@ -1,0 +1,121 @@
+"""GPU parity on the BASELINE.json workloads and on wide bitsets.
+
+* Wide bitsets (|P| > 1024 -> W = 64 / 128 words): K_n minus a perfect
+  matching on 2k of its vertices has exactly 2**k maximal cliques, each of
+  size n - k, and a degeneracy of n - 2 -- the first-level roots need the
+  widest bitset classes.  Checked bit-exactly against the oracle (count,
+  node total, histogram, hash) and against the closed form.
+* BASELINE workloads at sizes the oracle finishes in seconds: full runs for
+  er2k / ba200k, root samples (``root_begin/root_end/root_stride``) for the
+  R-MAT and planted-clique graphs, both sides on the SAME reordered graph.
+* Size-independent properties at full size where the oracle cannot follow:
+  first-level and second-level decompositions give the same clique set
+  (count, histogram, hash); the sharded runs sum to the whole.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2212_01473_b200 import RunConfig, from_edges, generate, preprocess, run
+from paper_2212_01473_b200.distributed import ShardResult, combine
+
+pytestmark = pytest.mark.gpu
+
+
+def k_minus_matching(n: int, k: int) -> np.ndarray:
+    u, v = np.triu_indices(n, k=1)
+    drop = (u < 2 * k) & (v == u + 1) & (u % 2 == 0)
+    return np.column_stack((u[~drop], v[~drop])).astype(np.int64)
+
+
+def _check_against_oracle(g2, st, roots="l1", induced="ipx", **kw):
+    res = run(g2, st, RunConfig(roots=roots, induced=induced, worker_list=False), **kw)
+    sample = {k: kw[k] for k in ("root_begin", "root_end", "root_stride") if k in kw}
+    inc = not sample
+    orc = oracle.enumerate_cliques(g2.row_offsets, g2.col_indices, roots=roots, induced=induced,
+                                   degeneracy=st.degeneracy, labels=g2.labels,
+                                   include_isolated=inc, **sample)
+    assert res.clique_count == orc["count"]
+    assert res.nodes_total == orc["nodes"]
+    assert res.clique_hash_hex == orc["hash"]
+    assert res.size_histogram == orc["hist"]
+    return res
+
+
+@pytest.mark.parametrize("n,k", [(1100, 6), (2150, 5)])
+def test_wide_bitsets_match_oracle_and_closed_form(n, k):
+    g = from_edges(k_minus_matching(n, k), n)
+    g2, _, st = preprocess(g)
+    assert st.degeneracy == n - 2 > 1024
+    # partial mode cannot pivot on X_X members: ~300x the nodes, oracle-bound
+    for induced in (("ipx", "ip") if n < 2048 else ("ipx",)):
+        res = _check_against_oracle(g2, st, induced=induced)
+        assert res.clique_count == 2 ** k
+        assert res.size_histogram == {n - k: 2 ** k}
+    # the worker list must not change the clique set
+    res = run(g2, st, RunConfig(donation_min_p=2))
+    assert res.clique_count == 2 ** k
+
+
+def test_capacity_error_beyond_widest_class():
+    from paper_2212_01473_b200 import CapacityError
+
+    n = 4200
+    g = from_edges(k_minus_matching(n, 1), n)
+    g2, _, st = preprocess(g)
+    with pytest.raises(CapacityError):
+        run(g2, st, RunConfig())
+
+
+@pytest.mark.parametrize("name", ["er2k", "ba200k"])
+def test_small_workloads_full_parity(name):
+    edges, n = generate.workload_edges(name)
+    g = from_edges(edges, n)
+    g2, _, st = preprocess(g)
+    res = _check_against_oracle(g2, st, induced="ipx")
+    ip = run(g2, st, RunConfig(induced="ip"))
+    assert (ip.clique_count, ip.clique_hash) == (res.clique_count, res.clique_hash)
+
+
+@pytest.mark.parametrize("name,sample", [
+    ("planted1m", dict(root_begin=0, root_end=-1, root_stride=97)),
+    ("planted1m", dict(root_begin=999_000, root_end=-1, root_stride=1)),
+    ("rmat20", dict(root_begin=0, root_end=600_000, root_stride=13)),
+])
+def test_large_workloads_sampled_parity(name, sample):
+    edges, n = generate.workload_edges(name)
+    g = from_edges(edges, n)
+    g2, _, st = preprocess(g)
+    _check_against_oracle(g2, st, induced="ipx", **sample)
+    _check_against_oracle(g2, st, induced="ip", **sample)
+
+
+def test_planted_full_l1_equals_l2_and_shards_sum():
+    edges, n = generate.workload_edges("planted1m")
+    g = from_edges(edges, n)
+    g2, _, st = preprocess(g)
+    whole = run(g2, st, RunConfig(worker_list=False))
+    # every planted clique (sizes 30-60) is maximal in a sparse background
+    assert sum(c for s, c in whole.size_histogram.items() if s >= 30) >= 990
+    l2 = run(g2, st, RunConfig(roots="l2"))
+    assert (l2.clique_count, l2.clique_hash, l2.size_histogram) == \
+        (whole.clique_count, whole.clique_hash, whole.size_histogram)
+    parts = []
+    for r in range(3):
+        p = run(g2, st, RunConfig(worker_list=False), root_begin=r, root_stride=3)
+        parts.append(ShardResult(p.clique_count, p.nodes_total, p.donation_count, p.clique_hash,
+                                 p.size_histogram))
+    tot = combine(parts)
+    assert tot.cliques == whole.clique_count and tot.hash == whole.clique_hash
+    assert tot.nodes == whole.nodes_total
+
+
+def test_from_edges_rejects_out_of_range_ids_on_device():
+    for bad in ([(0, 5)], [(-1, 2)], [(0, 1), (2, 3)]):
+        with pytest.raises(ValueError):
+            from_edges(np.asarray(bad, dtype=np.int64), 3 if bad != [(0, 5)] else 5)
+    g = from_edges(np.asarray([(0, 4), (4, 4)], dtype=np.int64), 5)  # self-loop dropped
+    assert g.num_edges == 1

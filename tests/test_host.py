@@ -145,3 +145,21 @@ def test_rmat_and_ba_generators_are_deterministic_and_in_range():
     ba = generate.barabasi_albert_edges(1000, 4, seed=1)
     assert ba.shape == (4000, 2) and ba.max() < 1000
     assert np.all(ba[:, 1] <= ba[:, 0])  # targets are earlier (or the source itself)
+
+
+def test_run_result_lazy_worker_metrics():
+    """RunResult keeps the device's per-worker rows raw and builds
+    WorkerMetrics objects on first access (host-only, no GPU)."""
+    import numpy as np
+
+    from paper_2212_01473_b200.scheduler import RunResult
+
+    raw = np.array([[5, 1, 0, 1], [7, 2, 1, 0]], dtype=np.int64)
+    res = RunResult(clique_count=3, donation_count=1, roots_mode="l1", induced_mode="ipx",
+                    workers=2, total_time=0.0, phase1_time=0.0, phase2_time=0.0,
+                    worker_metrics_raw=raw, nodes_total=12, timing=False)
+    wm = res.worker_metrics
+    assert [w.nodes_visited for w in wm] == [5, 7]
+    assert [w.donations_made for w in wm] == [0, 1]
+    assert res.report().nodes_total == 12 and res.report().load_ratio == pytest.approx(7 / 6)
+    assert res.worker_metrics is wm

@@ -1,4 +1,5 @@
-"""Ad-hoc diagnostics on the GPU box (not part of the product)."""
+"""Ad-hoc diagnostics on the GPU box (not part of the product).
+usage: python tools/diag.py <workload|don> [...] [--stride K]"""
 import sys, time, json, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -22,17 +23,23 @@ def donation_check():
                 wn = sum(w.nodes_visited for w in res.worker_metrics)
                 print(f"  workers={workers} wl={wl} count={res.clique_count} nodes={res.nodes_total} wnodes={wn} hash={res.clique_hash_hex} don={res.donation_count} made={made} recv={recv}")
 
-def timing(name):
+def timing(name, stride=1, reps=3, begin=0, end=-1):
     e, n = generate.workload_edges(name)
-    t = time.perf_counter(); g = from_edges(e, n); t1 = time.perf_counter()
-    o = degeneracy_order(g); t2 = time.perf_counter()
-    g2 = reorder(g, o); t3 = time.perf_counter()
-    st = stats(g2, o)
-    res = run(g2, st, RunConfig()); t4 = time.perf_counter()
-    res = run(g2, st, RunConfig()); t5 = time.perf_counter()
-    print(f"{name}: from_edges {t1-t:.4f}s order {t2-t1:.4f}s reorder {t3-t2:.4f}s run {t4-t3:.4f}s run2 {t5-t4:.4f}s count={res.clique_count} nodes={res.nodes_total} d={st.degeneracy} launches={res.kernel_launches} workers={res.workers} don={res.donation_count}")
+    for rep in range(reps):
+        t = time.perf_counter(); g = from_edges(e, n); t1 = time.perf_counter()
+        g2, o, st = preprocess(g); t2 = time.perf_counter()
+        res = run(g2, st, RunConfig(), root_stride=stride, root_begin=begin, root_end=end); t3 = time.perf_counter()
+        print(f"{name}[{rep}] roots[{begin}:{end}:{stride}]: from_edges {1e3*(t1-t):.2f}ms preprocess {1e3*(t2-t1):.2f}ms run {1e3*(t3-t2):.2f}ms "
+              f"(kernel {res.kernel_ms:.2f}ms) count={res.clique_count} nodes={res.nodes_total} d={st.degeneracy} "
+              f"maxdeg={st.max_degree} induced={res.induced_mode} launches={res.kernel_launches} workers={res.workers} "
+              f"don={res.donation_count} maxsize={res.max_clique_size}", flush=True)
 
 if __name__ == "__main__":
-    for a in sys.argv[1:]:
+    args = sys.argv[1:]
+    opt = {"stride": 1, "begin": 0, "end": -1, "reps": 3}
+    for k in list(opt):
+        if "--" + k in args:
+            i = args.index("--" + k); opt[k] = int(args[i + 1]); del args[i:i + 2]
+    for a in args:
         if a == "don": donation_check()
-        else: timing(a)
+        else: timing(a, **opt)

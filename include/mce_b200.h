@@ -98,6 +98,10 @@ typedef struct {
   int64_t collect_cap;   /* int64 words of the clique stream (0 = count only) */
   int64_t capacity_bits; /* bitset capacity; |P| above it -> -4 (0 = 1024) */
   double mem_fraction;   /* share of free HBM for per-worker scratch (0 -> 0.5) */
+  int measure_bytes;     /* also count the algorithmic CSR bytes of the induced-subgraph
+                            builds into mce_run_result.build_bytes (bench only; l1) */
+  int partial_xrows_min_w; /* partial mode: build X rows only for bitset classes of at
+                              least this many words (0 -> 4); same traversal either way */
 } mce_run_config;
 
 typedef struct {

@@ -38,6 +38,8 @@ class RunConfigC(ctypes.Structure):
         ("collect_cap", ctypes.c_int64),
         ("capacity_bits", ctypes.c_int64),
         ("mem_fraction", ctypes.c_double),
+        ("measure_bytes", ctypes.c_int),
+        ("partial_xrows_min_w", ctypes.c_int),
     ]
 
 

@@ -855,8 +855,9 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
 // every X member x) two offsets plus N+(a) (N+(x)).  out[0] = P part, out[1] = X part.
 __global__ void k_build_bytes(const int64_t* __restrict__ roots, int64_t count,
                               const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
-                              const int32_t* __restrict__ col, unsigned long long* __restrict__ out) {
-  unsigned long long bp = 0, bx = 0;
+                              const int32_t* __restrict__ col, int with_x,
+                              unsigned long long* __restrict__ out) {
+  unsigned long long bp = 0;
   const int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -868,19 +869,17 @@ __global__ void k_build_bytes(const int64_t* __restrict__ roots, int64_t count,
       const int32_t a = col[e];
       bp += 16 + 4 * (ro[a + 1] - split[a]);
     }
-    for (int64_t e = lo + lane; e < sp; e += 32) {
-      const int32_t x = col[e];
-      bx += 16 + 4 * (ro[x + 1] - split[x]);
+    if (with_x) {
+      for (int64_t e = lo + lane; e < sp; e += 32) {
+        const int32_t x = col[e];
+        bp += 16 + 4 * (ro[x + 1] - split[x]);
+      }
     }
   }
   typedef cub::BlockReduce<unsigned long long, 256> BR;
-  __shared__ typename BR::TempStorage t0, t1;
+  __shared__ typename BR::TempStorage t0;
   bp = BR(t0).Sum(bp);
-  bx = BR(t1).Sum(bx);
-  if (threadIdx.x == 0) {
-    atomicAdd(&out[0], bp);
-    atomicAdd(&out[1], bx);
-  }
+  if (threadIdx.x == 0) atomicAdd(out, bp);
 }
 
 __global__ void k_later_count(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
@@ -1062,12 +1061,15 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
 // HBM allows, still materialises the X rows so X_X adjacency is one bit test
 // instead of a binary search of the CSR -- same traversal tree, fewer
 // dependent loads.  Full mode ("ipx") always has them.
-int launch_mode(bool full, int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s,
-                int64_t* launches, size_t budget, int64_t resident_guess, cudaEvent_t* ev, bool* xr) {
+int launch_mode(bool full, int W, int xrows_min_w, EnumArgs args, int workers, int64_t* used,
+                cudaStream_t s, int64_t* launches, size_t budget, int64_t resident_guess,
+                cudaEvent_t* ev, bool* xr) {
   if (full) return launch_W<true, true>(W, args, workers, used, s, launches, budget, ev, xr);
   const size_t xrows_bytes = sizeof(uint32_t) * (size_t)W * (size_t)std::max<int64_t>(args.xcap, 1) *
                              (size_t)std::max<int64_t>(resident_guess, 1);
-  if (xrows_bytes <= budget / 2)
+  // small-|P| roots visit few nodes: building X rows (|X| x |N+(x)| loads)
+  // costs more than the CSR look-ups it saves
+  if (W >= xrows_min_w && xrows_bytes <= budget / 2)
     return launch_W<false, true>(W, args, workers, used, s, launches, budget, ev, xr);
   return launch_W<false, false>(W, args, workers, used, s, launches, budget, ev, xr);
 }
@@ -1143,10 +1145,16 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t launches = 0;
   int64_t trivial_nodes = 0;
   int64_t workers_used = 0;
-  double kernel_ms = 0.0;
-  int64_t build_bytes = 0;
   unsigned long long* bb = nullptr;
-  if (get(&bb, 2)) return -1;
+  if (get(&bb, 1)) return -1;
+  MCE_CHECK(cudaMemsetAsync(bb, 0, sizeof(unsigned long long), s));
+  cudaEvent_t events[2 * NUM_WIDTHS];
+  int nev = 0;
+  for (int e = 0; e < 2 * NUM_WIDTHS; ++e) cudaEventCreate(&events[e]);
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { for (int i = 0; i < 2 * NUM_WIDTHS; ++i) cudaEventDestroy(e[i]); }
+  } ev_guard{events};
   if (count > 0) {
     uint64_t *keys = nullptr, *keys2 = nullptr;
     int64_t *roots = nullptr, *roots2 = nullptr;
@@ -1232,32 +1240,20 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       int req = cfg->workers > 0 ? cfg->workers : 0;
       if (req <= 0) req = 0;
       const int64_t guess = req > 0 ? req : std::min<int64_t>(metric_slots, cp.count + metric_slots / 4);
-      cudaEvent_t ev[2];
-      cudaEventCreate(&ev[0]);
-      cudaEventCreate(&ev[1]);
+      cudaEvent_t* ev = &events[2 * nev++];
       bool xr = false;
-      int rc = launch_mode(cfg->induced_full != 0, cp.W, args, req, &workers_used, s, &launches,
-                           budget, guess, ev, &xr);
+      const int xmin = cfg->partial_xrows_min_w > 0 ? cfg->partial_xrows_min_w : 4;
+      int rc = launch_mode(cfg->induced_full != 0, cp.W, xmin, args, req, &workers_used, s,
+                           &launches, budget, guess, ev, &xr);
       if (rc) {
         cleanup();
         return rc;
       }
-      if (cfg->roots == 1) {
-        MCE_CHECK(cudaMemsetAsync(bb, 0, 2 * sizeof(unsigned long long), s));
+      if (cfg->measure_bytes && cfg->roots == 1) {  // measurement only (bench roofline)
         k_build_bytes<<<grid_for(cp.count * 32), 256, 0, s>>>(sorted_roots + cp.begin, cp.count,
-                                                               g->ro, g->split, g->col, bb);
+                                                               g->ro, g->split, g->col, xr, bb);
         mce_count_launch();
-        unsigned long long hb[2];
-        MCE_CHECK(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, s));
-        MCE_CHECK(cudaStreamSynchronize(s));
-        build_bytes += (int64_t)(hb[0] + (xr ? hb[1] : 0));
       }
-      MCE_CHECK(cudaEventSynchronize(ev[1]));
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[0], ev[1]);
-      kernel_ms += ms;
-      cudaEventDestroy(ev[0]);
-      cudaEventDestroy(ev[1]);
       wcap = std::max<int64_t>(wcap, req > 0 ? req : metric_slots);
     }
     max_workers_slots = std::max<int64_t>(workers_used, 1);
@@ -1285,7 +1281,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     MCE_CHECK(cudaGetLastError());
   }
   unsigned long long h_acc[8];
-  unsigned long long h_len = 0;
+  unsigned long long h_len = 0, h_bytes = 0;
+  MCE_CHECK(cudaMemcpyAsync(&h_bytes, bb, sizeof(h_bytes), cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaMemcpyAsync(h_acc, acc, sizeof(h_acc), cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaMemcpyAsync(out->hist, hist, sizeof(int64_t) * HIST_MAX, cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaMemcpyAsync(&h_len, collect_len, sizeof(h_len), cudaMemcpyDeviceToHost, s));
@@ -1312,8 +1309,14 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   out->workers = max_workers_slots;
   out->launches = launches;
   out->collect_len = (int64_t)h_len;
+  out->build_bytes = (int64_t)h_bytes;
+  double kernel_ms = 0.0;
+  for (int e = 0; e < nev; ++e) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, events[2 * e], events[2 * e + 1]);
+    kernel_ms += ms;
+  }
   out->kernel_ms = kernel_ms;
-  out->build_bytes = build_bytes;
   cleanup();
   return 0;
 }

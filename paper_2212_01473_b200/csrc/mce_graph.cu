@@ -675,10 +675,16 @@ int mce_graph_copy_csr(const mce_graph* g, int64_t* row_offsets, int64_t* col_in
 
 void mce_graph_free(mce_graph* g) {
   if (!g) return;
-  cudaFree(g->ro);
-  cudaFree(g->col);
-  cudaFree(g->split);
-  cudaFree(g->labels);
+  // stream-ordered frees back to the pool (everything was cudaMallocAsync'd):
+  // no device-wide synchronisation when a graph goes out of scope
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != g->device) cudaSetDevice(g->device);
+  if (g->ro) cudaFreeAsync(g->ro, 0);
+  if (g->col) cudaFreeAsync(g->col, 0);
+  if (g->split) cudaFreeAsync(g->split, 0);
+  if (g->labels) cudaFreeAsync(g->labels, 0);
+  if (cur != g->device) cudaSetDevice(cur);
   delete g;
 }
 

@@ -150,7 +150,7 @@ def _decode_stream(buf: np.ndarray, words: int, limit: int) -> list[tuple[int, .
 
 def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None, *,
         root_begin: int = 0, root_end: int = -1, root_stride: int = 1,
-        hash_labels: bool = True, stream=None) -> RunResult:
+        hash_labels: bool = True, stream=None, measure_bytes: bool = False) -> RunResult:
     """Enumerate all maximal cliques of a degeneracy-reordered graph on the
     GPU (reference scheduler.py:441-492).
 
@@ -187,6 +187,8 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
             collect_cap=cap_words,
             capacity_bits=0,
             mem_fraction=float(os.environ.get("MCE_MEM_FRACTION", "0.5")),
+            measure_bytes=int(bool(measure_bytes)),
+            partial_xrows_min_w=int(os.environ.get("MCE_PARTIAL_XROWS_MIN_W", "0")),
         )
         buf = np.zeros(max(cap_words, 1), dtype=np.int64) if cap_words else None
         wm = np.zeros((slots, 4), dtype=np.int64)

@@ -37,10 +37,29 @@ def test_ctypes_binding_covers_the_header():
     assert set(_lib.EXPORTS) == set(declared_functions())
 
 
+def _c_layout(struct: str, fields: list[str]) -> list[int]:
+    """sizeof + offsetof of every field, as gcc lays out the header's struct."""
+    import subprocess
+    import tempfile
+
+    body = "\n".join(f'printf("%zu\\n", offsetof({struct}, {f}));' for f in fields)
+    src = (f'#include <stddef.h>\n#include <stdio.h>\n#include "mce_b200.h"\n'
+           f'int main(void) {{ printf("%zu\\n", sizeof({struct})); {body} return 0; }}\n')
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "l.c"), os.path.join(d, "l")
+        with open(c, "w") as fh:
+            fh.write(src)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        return [int(x) for x in subprocess.run([exe], capture_output=True, text=True,
+                                               check=True).stdout.split()]
+
+
 def test_struct_layouts_match_header():
-    # mce_run_config: 6 ints, 3 int64, int, int64, int64, double (natural alignment)
-    assert ctypes.sizeof(_lib.RunConfigC) == 6 * 4 + 3 * 8 + 8 + 8 + 8 + 8
-    assert ctypes.sizeof(_lib.RunResultC) == 10 * 8 + 8 * _lib.HIST_MAX
+    for struct, cls in (("mce_run_config", _lib.RunConfigC), ("mce_run_result", _lib.RunResultC)):
+        names = [f[0] for f in cls._fields_]
+        want = _c_layout(struct, names)
+        got = [ctypes.sizeof(cls)] + [getattr(cls, f).offset for f in names]
+        assert got == want, struct
 
 
 def test_last_error_is_callable_without_a_device():

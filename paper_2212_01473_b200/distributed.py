@@ -1,13 +1,22 @@
 """Multi-GPU enumeration: first-level subtrees sharded across ranks.
 
 One process per GPU (``torch.distributed``).  The subtree roots are
-independent (paper §3.1), so ranks need no data-path communication: rank r
-enumerates the roots ``r, r + world, r + 2*world, ...`` of the degeneracy-
-reordered graph -- a static interleave over vertex ids, which spreads the
-heavy late-ordered roots evenly -- with its own device-wide worker list for
-intra-GPU balance.  The single collective is the final reduction of counts,
-node totals, size histograms and the order-independent clique-set hash
-(sum mod 2**64), done with one NCCL all-reduce (gloo on CPU tests).
+independent (paper §3.1), so ranks need no data-path communication.
+
+* ``run_sharded`` (static): rank r enumerates the roots ``r, r + world,
+  r + 2*world, ...`` of the degeneracy-reordered graph -- an interleave over
+  vertex ids, which spreads the heavy late-ordered roots evenly -- with its
+  own device-wide worker list for intra-GPU balance.
+* ``run_work_stealing`` (static + dynamic): the roots are cut into K
+  interleaved chunks ``{v : v % K == k}``; rank r first runs chunk r, then
+  claims further chunks off one shared counter (``store.add`` on the
+  process group's key-value store -- control plane only, a few bytes per
+  claim) until none are left, so a rank that drew light chunks keeps
+  working while another is still in a heavy one.
+
+Either way the single collective is the final reduction of counts, node
+totals, size histograms and the order-independent clique-set hash (sum mod
+2**64), done with one NCCL all-reduce (gloo in the CPU tests).
 """
 
 from __future__ import annotations
@@ -85,3 +94,46 @@ def run_sharded(g2, st, cfg: RunConfig, rank: int, world: int, device=None,
     if world == 1:
         return res, part
     return res, allreduce_result(part, device)
+
+
+_steal_epoch = 0
+
+
+def claim_chunks(store, key: str, rank: int, world: int, chunks: int):
+    """Chunk ids this rank runs: its static chunk ``rank`` first, then
+    chunks ``world, world+1, ...`` claimed off the shared counter ``key``
+    (each id handed out exactly once across ranks)."""
+    if rank < chunks:
+        yield rank
+    while True:
+        k = world + int(store.add(key, 1)) - 1
+        if k >= chunks:
+            return
+        yield k
+
+
+def run_work_stealing(g2, st, cfg: RunConfig, rank: int, world: int, chunks: int | None = None,
+                      device=None, store=None, runner=run,
+                      **kw) -> tuple[list[RunResult], ShardResult]:
+    """Static + dynamic sharding of the first-level roots (module docstring);
+    returns this rank's per-chunk results and the all-reduced totals."""
+    global _steal_epoch
+    import torch.distributed as dist
+
+    if cfg.roots == "l2":
+        raise ValueError("sharding is defined over first-level roots")
+    chunks = chunks or 4 * world
+    if chunks < world:
+        raise ValueError("need at least one chunk per rank")
+    if store is None:
+        store = dist.distributed_c10d._get_default_store()
+    _steal_epoch += 1  # every rank calls in the same order: same key per job
+    key = f"mce_steal_{_steal_epoch}"
+    results, parts = [], []
+    for k in claim_chunks(store, key, rank, world, chunks):
+        res = runner(g2, st, cfg, root_begin=k, root_end=-1, root_stride=chunks, **kw)
+        results.append(res)
+        parts.append(ShardResult(res.clique_count, res.nodes_total, res.donation_count,
+                                 res.clique_hash, res.size_histogram))
+    part = combine(parts) if parts else ShardResult(0, 0, 0, 0, {})
+    return results, (allreduce_result(part, device) if world > 1 else part)

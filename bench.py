@@ -61,6 +61,8 @@ def parse_args():
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--shard", default="static", choices=["static", "steal"],
+                   help="N>1: static interleave, or static + work-stealing chunks")
     return p.parse_args()
 
 
@@ -152,32 +154,41 @@ def load_workload(name: str, seed: int, on_device: bool):
     return generate.workload_edges(name, seed)
 
 
-def cpu_reference_step(ro, ci, root_stride: int, threads: int):
+def cpu_reference_step(ro, ci, root_stride: int, threads: int, pre=None):
     """The reference algorithm on host cores: exact degeneracy order,
     reorder, enumeration of a strided root sample (oracle/, C + numpy)."""
     from oracle import oracle
 
-    pos, d = oracle.degeneracy_order(ro, ci)
-    ro2, ci2 = oracle.reorder(ro, ci, pos)
+    ro2, ci2, d = pre if pre is not None else cpu_preprocess(ro, ci)
     n = len(ro) - 1
     max_degree = int(np.diff(ro2).max()) if n else 0
     induced = "ip" if d > 0 and max_degree / d > 200.0 else "ipx"
-    out = oracle.enumerate_cliques(ro2, ci2, roots="l1", induced=induced, degeneracy=d,
-                                   root_stride=root_stride, threads=threads)
-    return out
+    return oracle.enumerate_cliques(ro2, ci2, roots="l1", induced=induced, degeneracy=d,
+                                    root_stride=root_stride, threads=threads)
+
+
+def cpu_preprocess(ro, ci):
+    from oracle import oracle
+
+    pos, d = oracle.degeneracy_order(ro, ci)
+    ro2, ci2 = oracle.reorder(ro, ci, pos)
+    return ro2, ci2, d
 
 
 def choose_cpu_stride(ro, ci, target_s: float, threads: int) -> tuple[int, float, dict]:
-    """Pick a root stride so one CPU step costs about target_s seconds."""
-    stride = 1
-    probe = max(1, (len(ro) - 1) // 2000)
+    """Root stride so one CPU step (ordering + enumeration) costs about
+    target_s seconds: the ordering is timed once, the enumeration on a
+    1/64 probe sample."""
     t0 = time.perf_counter()
-    cpu_reference_step(ro, ci, probe, threads)
-    t_probe = time.perf_counter() - t0
-    est_full = t_probe * probe
-    if est_full > target_s:
-        stride = int(np.ceil(est_full / target_s))
-    return stride, t_probe, {}
+    pre = cpu_preprocess(ro, ci)
+    t_pre = time.perf_counter() - t0
+    probe = 64
+    t0 = time.perf_counter()
+    cpu_reference_step(ro, ci, probe, threads, pre)
+    est_enum = (time.perf_counter() - t0) * probe
+    budget = max(target_s - t_pre, 1.0)
+    stride = 1 if est_enum <= budget else int(np.ceil(est_enum / budget))
+    return stride, t_pre, {"est_enum_s": est_enum}
 
 
 def main():
@@ -195,7 +206,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2212_01473_b200 import RunConfig, from_device_edges, preprocess
     from paper_2212_01473_b200 import _lib
-    from paper_2212_01473_b200.distributed import run_sharded
+    from paper_2212_01473_b200.distributed import run_sharded, run_work_stealing
     from paper_2212_01473_b200.graph import from_edges
 
     _lib.require_device()
@@ -214,6 +225,13 @@ def main():
 
     def one_job(graph, measure=False):
         g2, _, st = preprocess(graph)
+        if world > 1 and stride == 1 and args.shard == "steal":
+            results, tot = run_work_stealing(g2, st, cfg, rank, world, device="cuda",
+                                             measure_bytes=measure)
+            res = results[0]
+            res.kernel_ms = sum(r.kernel_ms for r in results)
+            res.build_bytes = sum(r.build_bytes for r in results)
+            return res, tot, st
         if world > 1 or stride > 1:
             res, tot = run_sharded(g2, st, cfg, rank * 1, world * 1, device="cuda",
                                    measure_bytes=measure) \
@@ -298,7 +316,7 @@ def main():
                    "max_degree": st.max_degree, "roots": cfg.roots,
                    "induced": res.induced_mode, "root_stride": stride,
                    "maximal_cliques": count, "nodes": nodes, "clique_hash": chash,
-                   "ordering": "parallel peel",
+                   "ordering": "parallel peel", "sharding": args.shard if world > 1 else None,
                    "l2_flush": "256 MiB buffer zeroed between timed steps, outside the "
                                "CUDA events"},
         "e2e": ({"value": count / (e2e_ms / 1e3), "unit": "cliques/s", "ms_per_step": e2e_ms,

@@ -218,3 +218,33 @@ def reference_pipeline(edges, n: int, roots: str = "l1", induced: str = "auto",
     out.update({"n": n, "m": int(len(ci) // 2), "degeneracy": d, "max_degree": max_degree,
                 "induced": induced, "roots": roots})
     return out
+
+
+def bucket_peel_order(ro: np.ndarray, ci: np.ndarray) -> tuple[np.ndarray, int]:
+    """The GPU's ``method="parallel"`` ordering restated in numpy (NOT the
+    reference's; its exact order is ``degeneracy_order``): round-synchronous
+    bucket peeling -- at level k every live vertex with current degree <= k
+    leaves in the same round, ranked by id; an empty round raises k to
+    max(k + 1, min live degree); the degeneracy is the largest level at which
+    a round removed vertices."""
+    n = len(ro) - 1
+    deg = np.diff(ro).astype(np.int64)
+    alive = np.ones(n, dtype=bool)
+    pos = np.empty(n, dtype=np.int64)
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
+    k = 0
+    base = 0
+    dmax = 0
+    while base < n:
+        take = alive & (deg <= k)
+        if not take.any():
+            k = max(k + 1, int(deg[alive].min()))
+            continue
+        ids = np.flatnonzero(take)
+        pos[ids] = base + np.arange(len(ids))
+        base += len(ids)
+        dmax = max(dmax, k)
+        alive &= ~take
+        hit = take[src] & alive[ci]
+        np.subtract.at(deg, ci[hit], 1)
+    return pos, dmax

@@ -12,7 +12,8 @@ import os
 
 HIST_MAX = 4096
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmce_b200.so")
+# MCE_LIB_PATH: load an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("MCE_LIB_PATH") or os.path.join(_PKG, "libmce_b200.so")
 
 
 class MceError(RuntimeError):

@@ -141,7 +141,7 @@ struct Worker {
   uint32_t* rowsT;
   int32_t* plist;
   uint32_t* sP;
-  unsigned long long* s_hist;
+  unsigned int* s_hist;  // 32-bit CTA histogram (native shared atomics), spills at 2^31
   uint32_t* xrowsT;
   int32_t* xlist_buf;
   int32_t* xx;
@@ -159,7 +159,7 @@ struct Worker {
   bool phase2_seen = false;
 
   __device__ Worker(const EnumArgs& args, int lane_, int wid_, uint32_t* smem_rows,
-                    int32_t* smem_plist, uint32_t* smem_p, unsigned long long* smem_hist)
+                    int32_t* smem_plist, uint32_t* smem_p, unsigned int* smem_hist)
       : a(args), lane(lane_), wid(wid_), sP(smem_p), s_hist(smem_hist) {
     if (ROWS_SMEM) {
       rowsT = smem_rows;
@@ -451,7 +451,14 @@ struct Worker {
       cliques++;
       hash += mce_mix64(hs + (uint64_t)size * MCE_SIZE_SALT);
       if ((unsigned long long)size > max_size) max_size = size;
-      if (size < HIST_SMEM) atomicAdd(&s_hist[size], 1ull);
+      if (size < HIST_SMEM) {
+        // 64-bit shared atomics are CAS loops; count in 32 bits and move
+        // 2^31 to the global histogram whenever a counter reaches it
+        if (atomicAdd(&s_hist[size], 1u) == 0x7fffffffu) {
+          atomicAdd(&a.g_hist[size], 0x80000000ull);
+          atomicSub(&s_hist[size], 0x80000000u);
+        }
+      }
       else atomicAdd(&a.g_hist[size < HIST_MAX ? size : HIST_MAX - 1], 1ull);
     }
     if (a.collect_cap > 0) {
@@ -735,13 +742,24 @@ struct Worker {
   }
 };
 
+// Resident CTAs per SM the compiler must allow for (register budget).  The
+// narrow classes are latency-bound on dependent CSR loads: more resident
+// warps hide more of it.
+#ifndef MCE_MINB_SMALL
+#define MCE_MINB_SMALL 1
+#endif
+template <int W>
+struct MinBlocks {
+  static constexpr int value = W <= 4 ? MCE_MINB_SMALL : 1;
+};
+
 template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(EnumArgs a) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
   constexpr int SPW = W < 32 ? 32 : W;  // sP words per warp
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem);
+  unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem);
   uint32_t* s_p = reinterpret_cast<uint32_t*>(s_hist + HIST_SMEM);
   uint32_t* s_rows = s_p + WARPS * SPW;
   int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? WARPS * W * CAPP : 0));
@@ -783,7 +801,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_enumerate(EnumArgs a) {
   }
   __syncthreads();
   for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x)
-    if (s_hist[i]) atomicAdd(&a.g_hist[i], s_hist[i]);
+    if (s_hist[i]) atomicAdd(&a.g_hist[i], (unsigned long long)s_hist[i]);
 }
 
 // ------------------------------------------------------------ root prep
@@ -812,7 +830,7 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
                             int64_t count, uint64_t* __restrict__ keys,
                             int64_t* __restrict__ roots, unsigned long long* __restrict__ classes,
                             unsigned long long* __restrict__ max_p) {
-  __shared__ unsigned long long s_cls[TRIVIAL_RANK + 1];
+  __shared__ unsigned int s_cls[TRIVIAL_RANK + 1];
   if (threadIdx.x <= TRIVIAL_RANK) s_cls[threadIdx.x] = 0;
   __syncthreads();
   unsigned long long local_max = 0;
@@ -841,12 +859,14 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
     const uint64_t lim = (1ull << 56) - 1;
     if (cost > lim) cost = lim;
     keys[i] = ((uint64_t)rank << 56) | (lim - cost);
-    atomicAdd(&s_cls[rank], 1ull);
+    // warp-aggregated: one shared atomic per distinct class in the warp
+    const unsigned peers = __match_any_sync(__activemask(), rank);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_cls[rank], (unsigned)__popc(peers));
     if ((unsigned long long)p > local_max) local_max = p;
   }
   __syncthreads();
   if (threadIdx.x <= TRIVIAL_RANK && s_cls[threadIdx.x])
-    atomicAdd(&classes[threadIdx.x], s_cls[threadIdx.x]);
+    atomicAdd(&classes[threadIdx.x], (unsigned long long)s_cls[threadIdx.x]);
   if (local_max) atomicMax(max_p, local_max);
 }
 
@@ -966,7 +986,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   constexpr int CAPP = CAP + 1;
   auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
   constexpr int SPW = W < 32 ? 32 : W;
-  size_t smem = HIST_SMEM * sizeof(unsigned long long) + WARPS * SPW * sizeof(uint32_t) +
+  size_t smem = HIST_SMEM * sizeof(unsigned int) + WARPS * SPW * sizeof(uint32_t) +
                 (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
   MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0, per_sm = 0;

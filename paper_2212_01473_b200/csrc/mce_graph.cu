@@ -167,21 +167,33 @@ __global__ void k_split(const int64_t* __restrict__ ro, const int32_t* __restric
 // ---- parallel peel
 
 // ---- persistent parallel peel: the whole bucket-peeling loop in ONE
-// cooperative launch (no host round trip per round).  Round structure:
-//   1. each CTA scans its contiguous chunk of the alive list: how many have
-//      deg <= k ("take"), and the minimum alive degree;     grid sync
-//   2. every CTA reduces the per-CTA counts identically (so all CTAs take the
-//      same branch): nf == 0 -> k = max(k+1, min deg), next round;
-//      else rank the takes (base + exclusive prefix, alive-list = id order)
-//      and compact the keeps into the other alive buffer;   grid sync
-//   3. warps decrement the live neighbours of the frontier;  grid sync
-// Per-CTA counters are double-buffered by round parity: a CTA can run at
-// most one round ahead of the slowest (a grid sync separates them).
+// launch (software grid barrier; every CTA co-resident), no host round trip
+// per round.  Peel level k removes, round by round, every live vertex whose
+// current degree is <= k, ranking each round's removals by vertex id (so the
+// order is deterministic and identical to a round-synchronous bucket peel).
+//
+//  * FULL round (a level's first round, or a large one): every CTA scans its
+//    chunk of the alive list (ascending ids) for live vertices with
+//    deg <= k, counts them (and the minimum live degree), grid sync, ranks
+//    them by a grid-wide prefix and compacts the survivors.
+//  * INCREMENTAL round: after a productive round the next round's removals
+//    are exactly the vertices whose degree just crossed k+1 -> k; the
+//    decrement phase appends them to a crossing list (atomics, unordered)
+//    and CTA 0 sorts it by id (block radix sort, <= PEEL_SORT_MAX) -- no scan
+//    of the alive list at all.  Larger crossing sets fall back to FULL.
+//  * decrement: CTA-cooperative tiles of PEEL_TILE frontier vertices, their
+//    adjacency flattened over all threads (block scan of degrees + binary
+//    search for the owner), so a hub does not serialise one warp.
+// Two grid barriers per incremental round, three per full round.
 constexpr int PEEL_THREADS = 512;
+constexpr int PEEL_ITEMS = 8;
+constexpr int PEEL_SORT_MAX = PEEL_THREADS * PEEL_ITEMS;
+constexpr int PEEL_TILE = 256;
 
 struct PeelCounters {
   int64_t take[2];
   int32_t mindeg[2];
+  int64_t live[2];
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsigned int* gen,
@@ -195,33 +207,40 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsig
       __threadfence();
       atomicAdd((unsigned int*)gen, 1u);
     } else {
-      while (*gen == g) __nanosleep(32);
+      while (*gen == g) {
+      }
     }
     __threadfence();
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(PEEL_THREADS)
+__global__ void __launch_bounds__(PEEL_THREADS, 2)
 k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                   int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
-                  int32_t* __restrict__ frontier, uint8_t* __restrict__ removed,
-                  int64_t* __restrict__ pos, PeelCounters* __restrict__ blk,
-                  unsigned int* bar, int64_t* __restrict__ out_degeneracy) {
+                  int32_t* __restrict__ frontier, int32_t* __restrict__ cross,
+                  uint8_t* __restrict__ removed, int64_t* __restrict__ pos,
+                  PeelCounters* __restrict__ blk, unsigned int* bar,
+                  int64_t* __restrict__ out_degeneracy) {
   typedef cub::BlockReduce<int64_t, PEEL_THREADS> BRs;
   typedef cub::BlockReduce<int32_t, PEEL_THREADS> BRm;
   typedef cub::BlockScan<int32_t, PEEL_THREADS> BS;
+  typedef cub::BlockRadixSort<int32_t, PEEL_THREADS, PEEL_ITEMS> BSort;
   __shared__ union {
     typename BRs::TempStorage rs;
     typename BRm::TempStorage rm;
     typename BS::TempStorage sc;
+    typename BSort::TempStorage so;
   } tmp;
-  __shared__ int64_t s_nf, s_prefix;
+  __shared__ int64_t s_nf, s_prefix, s_live, s_live_prefix;
   __shared__ int32_t s_min;
+  __shared__ int64_t s_start[PEEL_TILE];
+  __shared__ int32_t s_off[PEEL_TILE + 1];
   const unsigned int G = gridDim.x;
   const int tid = threadIdx.x;
   unsigned int* bar_count = bar;
   volatile unsigned int* bar_gen = bar + 1;
+  unsigned int* ncross = bar + 2;  // [2], by parity
 
   for (int64_t v = blockIdx.x * (int64_t)PEEL_THREADS + tid; v < n; v += (int64_t)G * PEEL_THREADS) {
     deg[v] = (int32_t)(ro[v + 1] - ro[v]);
@@ -232,103 +251,191 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
 
   int32_t* alive = alive_a;
   int32_t* alive2 = alive_b;
-  int64_t na = n, base = 0;
+  int64_t na = n;       // alive-list length (may hold removed entries after incremental rounds)
+  int64_t left = n;     // vertices not yet ranked
+  int64_t base = 0;
   int32_t k = 0, deg_max = 0;
   int parity = 0;
-  while (na > 0) {
-    const int64_t chunk = (na + G - 1) / G;
-    const int64_t c0 = min((int64_t)blockIdx.x * chunk, na);
-    const int64_t c1 = min(c0 + chunk, na);
-    // 1. count takes and the minimum alive degree of this CTA's chunk
-    int64_t t = 0;
-    int32_t mn = 0x7fffffff;
-    for (int64_t i = c0 + tid; i < c1; i += PEEL_THREADS) {
-      const int32_t d = __ldcg(&deg[__ldcg(&alive[i])]);
-      t += (d <= k);
-      mn = min(mn, d);
-    }
-    t = BRs(tmp.rs).Sum(t);
-    __syncthreads();
-    mn = BRm(tmp.rm).Reduce(mn, cub::Min());
-    if (tid == 0) {
-      blk[blockIdx.x].take[parity] = t;
-      blk[blockIdx.x].mindeg[parity] = mn;
-    }
-    grid_barrier(bar_count, bar_gen, G);
-    // 2. identical reduction in every CTA
-    int64_t tot = 0, pre = 0;
-    int32_t gmin = 0x7fffffff;
-    for (unsigned int b = tid; b < G; b += PEEL_THREADS) {
-      const int64_t tb = __ldcg(&blk[b].take[parity]);
-      tot += tb;
-      if (b < blockIdx.x) pre += tb;
-      gmin = min(gmin, __ldcg(&blk[b].mindeg[parity]));
-    }
-    __syncthreads();
-    tot = BRs(tmp.rs).Sum(tot);
-    __syncthreads();
-    if (tid == 0) s_nf = tot;
-    __syncthreads();
-    pre = BRs(tmp.rs).Sum(pre);
-    __syncthreads();
-    gmin = BRm(tmp.rm).Reduce(gmin, cub::Min());
-    if (tid == 0) {
-      s_prefix = pre;
-      s_min = gmin;
-    }
-    __syncthreads();
-    const int64_t nf = s_nf;
-    parity ^= 1;
-    if (nf == 0) {
-      k = max(k + 1, s_min);
-      continue;
-    }
-    if (k > deg_max) deg_max = k;
-    // rank the takes in alive order, compact the keeps
-    int64_t run_take = s_prefix;            // takes before this tile, grid-wide
-    for (int64_t tile = c0; tile < c1; tile += PEEL_THREADS) {
-      const int64_t i = tile + tid;
-      int32_t v = 0, flag = 0;
-      if (i < c1) {
-        v = __ldcg(&alive[i]);
-        flag = __ldcg(&deg[v]) <= k;
+  bool incremental = false;
+  while (left > 0) {
+    int64_t nf;
+    if (incremental) {
+      nf = (int64_t)*(volatile unsigned int*)&ncross[parity];
+      if (nf == 0) {  // the level is exhausted
+        k += 1;
+        incremental = false;
+        continue;
       }
-      int32_t excl = 0, tile_total = 0;
-      BS(tmp.sc).ExclusiveSum(flag, excl, tile_total);
+      if (nf > PEEL_SORT_MAX) {
+        incremental = false;  // rank by a FULL scan instead (same set, same order)
+        continue;
+      }
+      if (k > deg_max) deg_max = k;
+      if (blockIdx.x == 0) {
+        int32_t keys[PEEL_ITEMS];
+#pragma unroll
+        for (int i = 0; i < PEEL_ITEMS; ++i) {
+          const int idx = tid * PEEL_ITEMS + i;
+          keys[i] = idx < nf ? __ldcg(&cross[(size_t)parity * n + idx]) : 0x7fffffff;
+        }
+        BSort(tmp.so).Sort(keys);
+#pragma unroll
+        for (int i = 0; i < PEEL_ITEMS; ++i) {
+          const int idx = tid * PEEL_ITEMS + i;
+          if (idx < nf) {
+            const int32_t v = keys[i];
+            frontier[idx] = v;
+            pos[v] = base + idx;
+            removed[v] = 1;
+          }
+        }
+        if (tid == 0) ncross[parity ^ 1] = 0;
+      }
+    } else {
+      // FULL: count live takes, live vertices and the minimum live degree
+      const int64_t chunk = (na + G - 1) / G;
+      const int64_t c0 = min((int64_t)blockIdx.x * chunk, na);
+      const int64_t c1 = min(c0 + chunk, na);
+      int64_t t = 0, lv = 0;
+      int32_t mn = 0x7fffffff;
+      for (int64_t i = c0 + tid; i < c1; i += PEEL_THREADS) {
+        const int32_t v = __ldcg(&alive[i]);
+        if (!__ldcg(&removed[v])) {
+          const int32_t d = __ldcg(&deg[v]);
+          t += (d <= k);
+          lv += 1;
+          mn = min(mn, d);
+        }
+      }
+      t = BRs(tmp.rs).Sum(t);
       __syncthreads();
-      if (i < c1) {
-        if (flag) {
-          const int64_t r = run_take + excl;
-          pos[v] = base + r;
-          frontier[r] = v;
-          removed[v] = 1;
-        } else {
-          alive2[i - run_take - excl] = v;  // keeps before i, grid-wide
-        }
+      lv = BRs(tmp.rs).Sum(lv);
+      __syncthreads();
+      mn = BRm(tmp.rm).Reduce(mn, cub::Min());
+      if (tid == 0) {
+        blk[blockIdx.x].take[parity] = t;
+        blk[blockIdx.x].live[parity] = lv;
+        blk[blockIdx.x].mindeg[parity] = mn;
       }
-      run_take += tile_total;
+      grid_barrier(bar_count, bar_gen, G);
+      int64_t tot = 0, pre = 0, ltot = 0, lpre = 0;
+      int32_t gmin = 0x7fffffff;
+      for (unsigned int b = tid; b < G; b += PEEL_THREADS) {
+        const int64_t tb = __ldcg(&blk[b].take[parity]);
+        const int64_t lb = __ldcg(&blk[b].live[parity]);
+        tot += tb;
+        ltot += lb;
+        if (b < blockIdx.x) {
+          pre += tb;
+          lpre += lb;
+        }
+        gmin = min(gmin, __ldcg(&blk[b].mindeg[parity]));
+      }
+      __syncthreads();
+      tot = BRs(tmp.rs).Sum(tot);
+      __syncthreads();
+      if (tid == 0) s_nf = tot;
+      __syncthreads();
+      pre = BRs(tmp.rs).Sum(pre);
+      __syncthreads();
+      if (tid == 0) s_prefix = pre;
+      __syncthreads();
+      lpre = BRs(tmp.rs).Sum(lpre);
+      __syncthreads();
+      if (tid == 0) s_live_prefix = lpre;
+      __syncthreads();
+      ltot = BRs(tmp.rs).Sum(ltot);
+      __syncthreads();
+      if (tid == 0) s_live = ltot;
+      __syncthreads();
+      gmin = BRm(tmp.rm).Reduce(gmin, cub::Min());
+      if (tid == 0) s_min = gmin;
+      __syncthreads();
+      nf = s_nf;
+      parity ^= 1;
+      if (nf == 0) {
+        k = max(k + 1, s_min);
+        continue;
+      }
+      if (k > deg_max) deg_max = k;
+      // rank the takes in alive (= id) order; compact the survivors
+      int64_t run_take = s_prefix;           // takes before this tile, grid-wide
+      int64_t run_live = s_live_prefix;      // live entries before this tile, grid-wide
+      for (int64_t tile = c0; tile < c1; tile += PEEL_THREADS) {
+        const int64_t i = tile + tid;
+        int32_t v = 0, isl = 0, flag = 0;
+        if (i < c1) {
+          v = __ldcg(&alive[i]);
+          isl = !__ldcg(&removed[v]);
+          flag = isl && __ldcg(&deg[v]) <= k;
+        }
+        // pack (take, live) into one scan: live < 2^16 per tile
+        int32_t excl = 0, tot_packed = 0;
+        BS(tmp.sc).ExclusiveSum(flag | (isl << 16), excl, tot_packed);
+        __syncthreads();
+        const int32_t ex_take = excl & 0xffff, ex_live = excl >> 16;
+        if (i < c1 && isl) {
+          if (flag) {
+            const int64_t r = run_take + ex_take;
+            pos[v] = base + r;
+            frontier[r] = v;
+            removed[v] = 1;
+          } else {
+            // survivors before v = live before v - takes before v
+            alive2[(run_live + ex_live) - (run_take + ex_take)] = v;
+          }
+        }
+        run_take += tot_packed & 0xffff;
+        run_live += tot_packed >> 16;
+      }
+      if (blockIdx.x == 0 && tid == 0) ncross[parity] = 0;
+      int32_t* t2 = alive;
+      alive = alive2;
+      alive2 = t2;
+      na = s_live - nf;
     }
     grid_barrier(bar_count, bar_gen, G);
-    // 3. decrement live neighbours of the frontier (one warp per vertex)
-    {
-      const int lane = tid & 31;
-      const int64_t warp = ((int64_t)blockIdx.x * PEEL_THREADS + tid) >> 5;
-      const int64_t nwarps = ((int64_t)G * PEEL_THREADS) >> 5;
-      for (int64_t f = warp; f < nf; f += nwarps) {
-        const int32_t v = __ldcg(&frontier[f]);
-        const int64_t e1 = ro[v + 1];
-        for (int64_t e = ro[v] + lane; e < e1; e += 32) {
-          const int32_t u = col[e];
-          if (!__ldcg(&removed[u])) atomicSub(&deg[u], 1);
+    // decrement: CTA-cooperative tiles of the frontier; crossers k+1 -> k
+    // go to the crossing list of the next round (parity after the flip)
+    const int np = incremental ? (parity ^ 1) : parity;
+    for (int64_t tile = (int64_t)blockIdx.x * PEEL_TILE; tile < nf; tile += (int64_t)G * PEEL_TILE) {
+      int32_t d = 0;
+      int64_t st = 0;
+      if (tid < PEEL_TILE && tile + tid < nf) {
+        const int32_t v = __ldcg(&frontier[tile + tid]);
+        st = ro[v];
+        d = (int32_t)(ro[v + 1] - st);
+      }
+      int32_t off = 0, total = 0;
+      BS(tmp.sc).ExclusiveSum(d, off, total);
+      if (tid < PEEL_TILE) {
+        s_start[tid] = st;
+        s_off[tid] = off;
+      }
+      if (tid == 0) s_off[PEEL_TILE] = total;
+      __syncthreads();
+      for (int32_t e = tid; e < total; e += PEEL_THREADS) {
+        int lo = 0, hi = PEEL_TILE;  // last owner with s_off[owner] <= e
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_off[mid] <= e) lo = mid; else hi = mid;
+        }
+        const int32_t u = col[s_start[lo] + (e - s_off[lo])];
+        if (!__ldcg(&removed[u])) {
+          const int32_t old = atomicSub(&deg[u], 1);
+          if (old == k + 1) {
+            const unsigned int slot = atomicAdd(&ncross[np], 1u);
+            cross[(size_t)np * n + slot] = u;
+          }
         }
       }
+      __syncthreads();
     }
     grid_barrier(bar_count, bar_gen, G);
-    int32_t* t2 = alive;
-    alive = alive2;
-    alive2 = t2;
+    if (incremental) parity ^= 1;
     base += nf;
-    na -= nf;
+    left -= nf;
+    incremental = true;
   }
   if (blockIdx.x == 0 && tid == 0) *out_degeneracy = deg_max;
 }
@@ -470,25 +577,28 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaS
     return -3;
   }
   // every CTA must be co-resident (software grid barrier)
-  int64_t grid = std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, (n + 4095) / 4096));
+  int64_t grid = std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, (n + 2047) / 2048));
   int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *frontier = nullptr;
+  int32_t* cross = nullptr;
   uint8_t* removed = nullptr;
   PeelCounters* blk = nullptr;
-  unsigned int* bar = nullptr;
+  unsigned int* bar = nullptr;  // barrier count, generation, crossing counters [2]
   int64_t* d_deg = nullptr;
   if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
-      dev_alloc(&frontier, n, s) || dev_alloc(&removed, n, s) || dev_alloc(&blk, grid, s) ||
-      dev_alloc(&bar, 2, s) || dev_alloc(&d_deg, 1, s))
+      dev_alloc(&frontier, n, s) || dev_alloc(&cross, 2 * n, s) || dev_alloc(&removed, n, s) ||
+      dev_alloc(&blk, grid, s) || dev_alloc(&bar, 4, s) || dev_alloc(&d_deg, 1, s))
     return -1;
-  MCE_CHECK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s));
+  MCE_CHECK(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned int), s));
   k_peel_persistent<<<(int)grid, PEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2,
-                                                      frontier, removed, d_pos, blk, bar, d_deg);
+                                                      frontier, cross, removed, d_pos, blk, bar,
+                                                      d_deg);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaStreamSynchronize(s));
   dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(frontier, s);
-  dev_free(removed, s); dev_free(blk, s); dev_free(bar, s); dev_free(d_deg, s);
+  dev_free(cross, s); dev_free(removed, s); dev_free(blk, s); dev_free(bar, s);
+  dev_free(d_deg, s);
   return 0;
 }
 

@@ -43,6 +43,8 @@ def test_csr_and_orderings_match_reference(case):
     assert exact.position.tolist() == case["position"]
     par = degeneracy_order(g, method="parallel")
     assert par.degeneracy == case["degeneracy"]
+    bpos, _ = oracle.bucket_peel_order(ro, ci)
+    assert np.array_equal(par.position, bpos)
     assert sorted(par.position.tolist()) == list(range(case["n"]))
     g2 = reorder(g, par)
     n = case["n"]

@@ -119,3 +119,20 @@ def test_from_edges_rejects_out_of_range_ids_on_device():
             from_edges(np.asarray(bad, dtype=np.int64), 3 if bad != [(0, 5)] else 5)
     g = from_edges(np.asarray([(0, 4), (4, 4)], dtype=np.int64), 5)  # self-loop dropped
     assert g.num_edges == 1
+
+
+@pytest.mark.parametrize("name", ["er2k", "ba200k", "planted1m"])
+def test_parallel_peel_positions_match_restatement(name):
+    """The persistent peel kernel (incremental + full rounds) reproduces the
+    round-synchronous bucket peel exactly: positions and degeneracy."""
+    from paper_2212_01473_b200 import degeneracy_order
+
+    edges, n = generate.workload_edges(name)
+    g = from_edges(edges, n)
+    got = degeneracy_order(g, method="parallel")
+    pos, d = oracle.bucket_peel_order(g.row_offsets, g.col_indices)
+    assert got.degeneracy == d
+    assert np.array_equal(got.position, pos)
+    # preprocess (device-resident positions) agrees with the host-visible order
+    _, order, st = preprocess(g)
+    assert np.array_equal(order.position, pos) and st.degeneracy == d

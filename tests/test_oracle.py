@@ -63,3 +63,19 @@ def test_hash_is_order_independent():
     b = oracle.summarize_cliques([(5, 4), (3, 1, 2)])
     assert a == b
     assert oracle.clique_hash([1, 2]) != oracle.clique_hash([1, 3])
+
+
+def test_bucket_peel_order_is_a_degeneracy_order():
+    """The parallel-order restatement (checker of the GPU peel) yields the
+    reference's degeneracy on every golden graph and a valid permutation."""
+    from conftest import golden_cases
+
+    for case in golden_cases():
+        edges = np.asarray(case["edges"], dtype=np.int64).reshape(-1, 2)
+        ro, ci = oracle.from_edges(edges, case["n"])
+        pos, d = oracle.bucket_peel_order(ro, ci)
+        assert d == case["degeneracy"]
+        assert sorted(pos.tolist()) == list(range(case["n"]))
+        ro2, ci2 = oracle.reorder(ro, ci, pos)
+        later = [int(np.sum(ci2[ro2[v]:ro2[v + 1]] > v)) for v in range(case["n"])]
+        assert max(later, default=0) == d

@@ -264,7 +264,9 @@ def main():
             kernel_ms += res.kernel_ms
         torch.cuda.synchronize()
     launches = _lib.lib().mce_launch_count() - launches0
-    dev_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    dev_ms = sum(step_ms) / args.steps
+    print(f"[bench] per-step device ms: {[round(x, 3) for x in step_ms]}", file=sys.stderr)
     count = tot.cliques if tot is not None else res.clique_count
     nodes = tot.nodes if tot is not None else res.nodes_total
     chash = f"{tot.hash:016x}" if tot is not None else res.clique_hash_hex

@@ -133,6 +133,7 @@ struct Worker {
   static constexpr int CAP = 32 * W;
   static constexpr int CAPP = CAP + 1;
   static constexpr int K = (W + 31) / 32;
+  static constexpr int SPW = W < 32 ? 32 : W;
   using B = Bits<W>;
 
   const EnumArgs& a;
@@ -140,7 +141,9 @@ struct Worker {
   const int wid;
   uint32_t* rowsT;
   int32_t* plist;
-  uint32_t* sP;
+  uint32_t* sP;   // the node's P, X_P and branch set, broadcast words (SPW each)
+  uint32_t* sXP;
+  uint32_t* sBR;
   unsigned int* s_hist;  // 32-bit CTA histogram (native shared atomics), spills at 2^31
   uint32_t* xrowsT;
   int32_t* xlist_buf;
@@ -160,7 +163,8 @@ struct Worker {
 
   __device__ Worker(const EnumArgs& args, int lane_, int wid_, uint32_t* smem_rows,
                     int32_t* smem_plist, uint32_t* smem_p, unsigned int* smem_hist)
-      : a(args), lane(lane_), wid(wid_), sP(smem_p), s_hist(smem_hist) {
+      : a(args), lane(lane_), wid(wid_), sP(smem_p), sXP(smem_p + SPW), sBR(smem_p + 2 * SPW),
+        s_hist(smem_hist) {
     if (ROWS_SMEM) {
       rowsT = smem_rows;
       plist = smem_plist;
@@ -172,7 +176,7 @@ struct Worker {
     xlist_buf = a.xlist ? a.xlist + (size_t)wid * a.xcap : nullptr;
     xx = a.xx + (size_t)wid * a.xcap;
     xtmp = a.xtmp + (size_t)wid * a.xcap;
-    stk = a.stack + (size_t)wid * a.levels * 3 * W;
+    stk = a.stack + (size_t)wid * a.levels * 4 * W;
     lpx = a.lpx + (size_t)wid * a.levels;
     rpath = a.rpath + (size_t)wid * (a.levels + 2);
     hsum = a.hsum + (size_t)wid * (a.levels + 2);
@@ -451,15 +455,7 @@ struct Worker {
       cliques++;
       hash += mce_mix64(hs + (uint64_t)size * MCE_SIZE_SALT);
       if ((unsigned long long)size > max_size) max_size = size;
-      if (size < HIST_SMEM) {
-        // 64-bit shared atomics are CAS loops; count in 32 bits and move
-        // 2^31 to the global histogram whenever a counter reaches it
-        if (atomicAdd(&s_hist[size], 1u) == 0x7fffffffu) {
-          atomicAdd(&a.g_hist[size], 0x80000000ull);
-          atomicSub(&s_hist[size], 0x80000000u);
-        }
-      }
-      else atomicAdd(&a.g_hist[size < HIST_MAX ? size : HIST_MAX - 1], 1ull);
+      hist_add(size, 1u);  // 32-bit shared counters (64-bit shared atomics are CAS loops)
     }
     if (a.collect_cap > 0) {
       unsigned long long pos = 0;
@@ -471,6 +467,129 @@ struct Worker {
         for (int i = lane; i < size; i += 32) a.collect[pos + 1 + i] = rpath[i];
       }
     }
+  }
+
+  __device__ __forceinline__ void hist_add(int size, unsigned cnt) {
+    if (size < HIST_SMEM) {
+      const unsigned old = atomicAdd(&s_hist[size], cnt);
+      if (old < 0x80000000u && old + cnt >= 0x80000000u) {  // spill 2^31 to HBM
+        atomicAdd(&a.g_hist[size], 0x80000000ull);
+        atomicSub(&s_hist[size], 0x80000000u);
+      }
+    } else {
+      atomicAdd(&a.g_hist[size < HIST_MAX ? size : HIST_MAX - 1], (unsigned long long)cnt);
+    }
+  }
+
+  // Leaf batch (the sibling subtrees of a node are independent given the
+  // node's P, X_P, branch set BR and live X_X prefix): every branch v whose
+  // child P_v & N(v) is empty -- P_v = P minus the branches before v -- is a
+  // leaf of the reference's traversal (scheduler.py:358-369).  All of them
+  // are decided in one lane-per-candidate pass: node count += #leaves, the
+  // maximal ones (X_v & N(v) empty, X_v = X_P plus the earlier branches, and
+  // no live X_X neighbour) are reported together.  Returns BR minus leaves.
+  __device__ void leaf_batch(const B& P, const B& XP, const B& BR, int live, int rlen, B& NL) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (valid(k, lane)) {
+        sXP[word(k)] = XP.w[k];
+        sBR[word(k)] = BR.w[k];
+      }
+      NL.w[k] = BR.w[k];
+    }
+    unsigned umask[K];  // words where P | X_P has bits: the only row words that matter
+#pragma unroll
+    for (int k = 0; k < K; ++k) umask[k] = __ballot_sync(FULLMASK, (P.w[k] | XP.w[k]) != 0);
+    __syncwarp();
+    const uint64_t hs = hsum[rlen];
+    const int size = rlen + 1;
+    unsigned long long hsum_lane = 0;
+    unsigned leaves = 0, maximal = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      for (unsigned bm = __ballot_sync(FULLMASK, BR.w[k] != 0); bm; bm &= bm - 1) {
+        const int fl = __ffs(bm) - 1;
+        const int w = k * 32 + fl;  // candidate word: candidate c = 32w + lane
+        const uint32_t bw = __shfl_sync(FULLMASK, BR.w[k], fl);
+        const bool cand = (bw >> lane) & 1u;
+        const int c = (w << 5) + lane;
+        bool leaf = false, xclear = false;
+        if (cand) {
+          uint32_t pin = 0, xin = 0;
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            for (unsigned um = umask[q]; um; um &= um - 1) {
+              const int j = q * 32 + __ffs(um) - 1;
+              const uint32_t below = j < w ? 0xffffffffu : (j == w ? (1u << lane) - 1u : 0u);
+              const uint32_t r = rowsT[j * CAPP + c];
+              const uint32_t bb = sBR[j] & below;
+              pin |= r & (sP[j] & ~bb);
+              xin |= r & (sXP[j] | bb);
+            }
+          }
+          leaf = pin == 0;
+          xclear = leaf && xin == 0;
+        }
+        const unsigned lm = __ballot_sync(FULLMASK, leaf);
+        if (!lm) continue;
+        leaves += __popc(lm);
+        // drop the leaves from the non-leaf branch set (word w lives in lane fl, slot k)
+        if (lane == fl) NL.w[k] &= ~lm;
+        unsigned xm = __ballot_sync(FULLMASK, xclear);
+        if (xm && live > 0) {
+          if (XROWS) {
+            uint32_t adj = 0;  // live X_X members' adjacency, word w
+            for (int i = lane; i < live; i += 32) adj |= xrowsT[(size_t)w * a.xcap + xx[i]];
+            adj = __reduce_or_sync(FULLMASK, adj);
+            xm &= ~adj;
+          } else {
+            for (unsigned t = xm; t; t &= t - 1) {
+              const int b = __ffs(t) - 1;
+              const int v = (w << 5) + b;
+              if (xx_any_adjacent(v, plist[v], live)) xm &= ~(1u << b);
+            }
+          }
+        }
+        if (!xm) continue;
+        if ((xm >> lane) & 1u) {
+          hsum_lane += mce_mix64(hs + a.vhash[plist[c]] + (uint64_t)size * MCE_SIZE_SALT);
+        }
+        maximal += __popc(xm);
+        if (a.collect_cap > 0) {
+          for (unsigned t = xm; t; t &= t - 1) {
+            const int v = (w << 5) + __ffs(t) - 1;
+            collect_clique(size, plist[v]);
+          }
+        }
+      }
+    }
+    nodes += leaves;
+    if (maximal) {
+      // 64-bit warp sum of the per-lane hashes
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) hsum_lane += __shfl_xor_sync(FULLMASK, hsum_lane, o);
+      if (lane == 0) {
+        cliques += maximal;
+        hash += hsum_lane;
+        if ((unsigned long long)size > max_size) max_size = size;
+        hist_add(size, maximal);
+      }
+    }
+  }
+
+  // append [size, R..., last] to the clique stream (collect mode)
+  __device__ void collect_clique(int size, int32_t last) {
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(a.collect_len, (unsigned long long)(size + 1));
+    pos = __shfl_sync(FULLMASK, pos, 0);
+    if (pos + size + 1 <= (unsigned long long)a.collect_cap) {
+      if (lane == 0) {
+        a.collect[pos] = size;
+        a.collect[pos + size] = last;
+      }
+      for (int i = lane; i < size - 1; i += 32) a.collect[pos + 1 + i] = rpath[i];
+    }
+    __syncwarp();
   }
 
   __device__ bool phase2() {
@@ -583,28 +702,35 @@ struct Worker {
   }
 
   // ---------------------------------------------------------------- DFS
-  __device__ __forceinline__ void push(int depth, const B& P, const B& XP, const B& BR) {
-    uint32_t* f = stk + (size_t)depth * 3 * W;
+  // frame: P, X_P, remaining branches BR, remaining non-leaf branches NL
+  __device__ __forceinline__ void push(int depth, const B& P, const B& XP, const B& BR,
+                                       const B& NL) {
+    uint32_t* f = stk + (size_t)depth * 4 * W;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       if (valid(k, lane)) {
         f[word(k)] = P.w[k];
         f[W + word(k)] = XP.w[k];
         f[2 * W + word(k)] = BR.w[k];
+        f[3 * W + word(k)] = NL.w[k];
       }
     }
   }
-  __device__ __forceinline__ void pop(int depth, B& P, B& XP, B& BR) const {
-    const uint32_t* f = stk + (size_t)depth * 3 * W;
+  __device__ __forceinline__ void pop(int depth, B& P, B& XP, B& BR, B& NL) const {
+    const uint32_t* f = stk + (size_t)depth * 4 * W;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       P.w[k] = valid(k, lane) ? f[word(k)] : 0u;
       XP.w[k] = valid(k, lane) ? f[W + word(k)] : 0u;
       BR.w[k] = valid(k, lane) ? f[2 * W + word(k)] : 0u;
+      NL.w[k] = valid(k, lane) ? f[3 * W + word(k)] : 0u;
     }
   }
 
   // Traverse from the level-0 state (P, XP, xx[0, nxx), rpath[0, rlen)).
+  // Leaves are settled per node by leaf_batch; the loop walks the non-leaf
+  // branches in the reference's order, applying the P -> X_P moves of the
+  // leaf branches that precede each one.
   __device__ void traverse(B P, B XP, int nxx, int rlen) {
     uint64_t hs = 0;
     for (int i = 0; i < rlen; ++i) hs += a.vhash[rpath[i]];
@@ -614,36 +740,40 @@ struct Worker {
       return;
     }
     int depth = 0;
-    int below = 0;  // frozen frames with branches left (scheduler.py:346-348)
+    int below = 0;  // frozen frames with (non-leaf) branches left (scheduler.py:346-348)
     if (lane == 0) {
       lpx[0] = nxx;
       hsum[rlen] = hs;
     }
     int live = nxx;
     nodes++;
-    B BR;
+    B BR, NL;
     pivot_branches(P, XP, live, BR);
+    leaf_batch(P, XP, BR, live, rlen, NL);
     for (;;) {
-      const int v = first(BR);
+      const int v = first(NL);
       if (v < 0) {
         if (depth == 0) break;
         depth--;
         rlen--;
-        pop(depth, P, XP, BR);
-        if (any(BR)) below--;
+        pop(depth, P, XP, BR, NL);
+        if (any(NL)) below--;
         live = lpx[depth];
         continue;
       }
       {
-        const int kv = v >> 10, lv = (v >> 5) & 31;
+        // move v and the (leaf) branches before it from P to X_P
+        const int wv = v >> 5;
         const uint32_t bit = 1u << (v & 31);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if (k == kv && lane == lv) {
-            BR.w[k] &= ~bit;
-            P.w[k] &= ~bit;
-            XP.w[k] |= bit;
-          }
+          const int wd = word(k);
+          const uint32_t below_m = wd < wv ? 0xffffffffu : (wd == wv ? bit - 1u : 0u);
+          const uint32_t m = (BR.w[k] & below_m) | (wd == wv ? bit : 0u);
+          BR.w[k] &= ~m;
+          NL.w[k] &= ~m;
+          P.w[k] &= ~m;
+          XP.w[k] |= m;
         }
       }
       B rowv, childP;
@@ -652,13 +782,13 @@ struct Worker {
       for (int k = 0; k < K; ++k) childP.w[k] = P.w[k] & rowv.w[k];
       const int cpop = popc(childP);
       const int32_t gv = plist[v];
-      if (a.worker_list_on && cpop >= a.min_p && below > 0 && any(BR) && phase2()) {
+      if (a.worker_list_on && cpop >= a.min_p && below > 0 && any(NL) && phase2()) {
         B cxp;
 #pragma unroll
         for (int k = 0; k < K; ++k) cxp.w[k] = XP.w[k] & rowv.w[k];
         if (try_donate(childP, cxp, v, gv, live, rlen)) continue;
       }
-      if (cpop == 0) {  // scheduler.py:358-369
+      if (cpop == 0) {  // not reached: leaf_batch settled every leaf branch
         nodes++;
         uint32_t o = 0;
 #pragma unroll
@@ -673,8 +803,8 @@ struct Worker {
         continue;
       }
       const int kept = partition(v, gv, live);
-      push(depth, P, XP, BR);
-      if (any(BR)) below++;
+      push(depth, P, XP, BR, NL);
+      if (any(NL)) below++;
       depth++;
       live = kept;
 #pragma unroll
@@ -691,6 +821,7 @@ struct Worker {
       nodes++;
       __syncwarp();
       pivot_branches(P, XP, live, BR);
+      leaf_batch(P, XP, BR, live, rlen, NL);
     }
   }
 
@@ -746,7 +877,7 @@ struct Worker {
 // narrow classes are latency-bound on dependent CSR loads: more resident
 // warps hide more of it.
 #ifndef MCE_MINB_SMALL
-#define MCE_MINB_SMALL 1
+#define MCE_MINB_SMALL 4
 #endif
 template <int W>
 struct MinBlocks {
@@ -761,7 +892,7 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem);
   uint32_t* s_p = reinterpret_cast<uint32_t*>(s_hist + HIST_SMEM);
-  uint32_t* s_rows = s_p + WARPS * SPW;
+  uint32_t* s_rows = s_p + 3 * WARPS * SPW;
   int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? WARPS * W * CAPP : 0));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -770,7 +901,7 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
   const int wid = blockIdx.x * WARPS + warp;
   if (wid < a.num_workers) {
     Worker<W, PIVOT_XX, XROWS, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
-                                  s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + warp * SPW,
+                                  s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + 3 * warp * SPW,
                                   s_hist);
     for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-273)
       unsigned long long idx = 0;
@@ -986,7 +1117,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   constexpr int CAPP = CAP + 1;
   auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
   constexpr int SPW = W < 32 ? 32 : W;
-  size_t smem = HIST_SMEM * sizeof(unsigned int) + WARPS * SPW * sizeof(uint32_t) +
+  size_t smem = HIST_SMEM * sizeof(unsigned int) + 3 * WARPS * SPW * sizeof(uint32_t) +
                 (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
   MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0, per_sm = 0;
@@ -1002,7 +1133,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   // DFS depth <= |P| of the root: the class's stack never exceeds min(CAP, max |P|)
   const int64_t levels = std::min<int64_t>(CAP, std::max<int64_t>(args.levels, 1)) + 3;
   const int64_t xcap = std::max<int64_t>(args.xcap, 1);
-  size_t per_worker = sizeof(uint32_t) * (size_t)(levels * 3 * W) + sizeof(int32_t) * levels +
+  size_t per_worker = sizeof(uint32_t) * (size_t)(levels * 4 * W) + sizeof(int32_t) * levels +
                       (sizeof(int32_t) + sizeof(uint64_t)) * (levels + 2) +
                       sizeof(int32_t) * 2 * xcap + sizeof(Mailbox) + sizeof(uint32_t) * 2 * W +
                       sizeof(int) * 2 +
@@ -1026,7 +1157,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
     owned.push_back((void*)*p);
     return 0;
   };
-  if (get(&args.stack, (size_t)workers * levels * 3 * W) || get(&args.lpx, (size_t)workers * levels) ||
+  if (get(&args.stack, (size_t)workers * levels * 4 * W) || get(&args.lpx, (size_t)workers * levels) ||
       get(&args.rpath, (size_t)workers * (levels + 2)) || get(&args.hsum, (size_t)workers * (levels + 2)) ||
       get(&args.xx, (size_t)workers * xcap) || get(&args.xtmp, (size_t)workers * xcap) ||
       get(&args.mbox, (size_t)workers) || get(&args.mbits, (size_t)workers * 2 * W) ||

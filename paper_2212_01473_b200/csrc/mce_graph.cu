@@ -215,7 +215,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsig
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(PEEL_THREADS, 2)
+__global__ void __launch_bounds__(PEEL_THREADS)
 k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                   int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
                   int32_t* __restrict__ frontier, int32_t* __restrict__ cross,
@@ -226,11 +226,13 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
   typedef cub::BlockReduce<int32_t, PEEL_THREADS> BRm;
   typedef cub::BlockScan<int32_t, PEEL_THREADS> BS;
   typedef cub::BlockRadixSort<int32_t, PEEL_THREADS, PEEL_ITEMS> BSort;
+  typedef cub::BlockRadixSort<int32_t, PEEL_THREADS, 1> BSort1;
   __shared__ union {
     typename BRs::TempStorage rs;
     typename BRm::TempStorage rm;
     typename BS::TempStorage sc;
     typename BSort::TempStorage so;
+    typename BSort1::TempStorage so1;
   } tmp;
   __shared__ int64_t s_nf, s_prefix, s_live, s_live_prefix;
   __shared__ int32_t s_min;
@@ -241,6 +243,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
   unsigned int* bar_count = bar;
   volatile unsigned int* bar_gen = bar + 1;
   unsigned int* ncross = bar + 2;  // [2], by parity
+  const int id_bits = n > 1 ? 32 - __clz((int)(n - 1)) : 1;
 
   for (int64_t v = blockIdx.x * (int64_t)PEEL_THREADS + tid; v < n; v += (int64_t)G * PEEL_THREADS) {
     deg[v] = (int32_t)(ro[v + 1] - ro[v]);
@@ -272,21 +275,42 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
       }
       if (k > deg_max) deg_max = k;
       if (blockIdx.x == 0) {
-        int32_t keys[PEEL_ITEMS];
-#pragma unroll
-        for (int i = 0; i < PEEL_ITEMS; ++i) {
-          const int idx = tid * PEEL_ITEMS + i;
-          keys[i] = idx < nf ? __ldcg(&cross[(size_t)parity * n + idx]) : 0x7fffffff;
-        }
-        BSort(tmp.so).Sort(keys);
-#pragma unroll
-        for (int i = 0; i < PEEL_ITEMS; ++i) {
-          const int idx = tid * PEEL_ITEMS + i;
-          if (idx < nf) {
-            const int32_t v = keys[i];
-            frontier[idx] = v;
-            pos[v] = base + idx;
+        const int32_t* cl = cross + (size_t)parity * n;
+        if (nf == 1) {
+          if (tid == 0) {
+            const int32_t v = __ldcg(&cl[0]);
+            frontier[0] = v;
+            pos[v] = base;
             removed[v] = 1;
+          }
+        } else if (nf <= PEEL_THREADS) {
+          // ids are < n <= 2^id_bits: sort only those bits (fewer passes);
+          // the stable sort keeps the all-ones padding after real ids
+          const int32_t pad = (int32_t)((1u << id_bits) - 1u);
+          int32_t key[1] = {tid < nf ? __ldcg(&cl[tid]) : pad};
+          BSort1(tmp.so1).Sort(key, 0, id_bits);
+          if (tid < nf) {
+            frontier[tid] = key[0];
+            pos[key[0]] = base + tid;
+            removed[key[0]] = 1;
+          }
+        } else {
+          int32_t keys[PEEL_ITEMS];
+#pragma unroll
+          for (int i = 0; i < PEEL_ITEMS; ++i) {
+            const int idx = tid * PEEL_ITEMS + i;
+            keys[i] = idx < nf ? __ldcg(&cl[idx]) : 0x7fffffff;
+          }
+          BSort(tmp.so).Sort(keys);
+#pragma unroll
+          for (int i = 0; i < PEEL_ITEMS; ++i) {
+            const int idx = tid * PEEL_ITEMS + i;
+            if (idx < nf) {
+              const int32_t v = keys[i];
+              frontier[idx] = v;
+              pos[v] = base + idx;
+              removed[v] = 1;
+            }
           }
         }
         if (tid == 0) ncross[parity ^ 1] = 0;

@@ -27,6 +27,8 @@ def timing(name, stride=1, reps=3, begin=0, end=-1):
     e, n = generate.workload_edges(name)
     for rep in range(reps):
         t = time.perf_counter(); g = from_edges(e, n); t1 = time.perf_counter()
+        tp = time.perf_counter(); degeneracy_order(g); tp = time.perf_counter() - tp
+        print(f"  degeneracy_order(parallel) {1e3*tp:.2f}ms", flush=True)
         g2, o, st = preprocess(g); t2 = time.perf_counter()
         res = run(g2, st, RunConfig(), root_stride=stride, root_begin=begin, root_end=end); t3 = time.perf_counter()
         print(f"{name}[{rep}] roots[{begin}:{end}:{stride}]: from_edges {1e3*(t1-t):.2f}ms preprocess {1e3*(t2-t1):.2f}ms run {1e3*(t3-t2):.2f}ms "

@@ -41,8 +41,8 @@ for r in rows[2:]:
             vals[h] = (r[i], units[i])
     for h in sorted(vals):
         print(f"  {h:75s} {vals[h][0]:>18s} {vals[h][1]}")
-    SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-             "msecond": 1e6, "second": 1e9}
+    SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "ns": 1,
+             "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9, "s": 1e9}
 
     def f(k):  # bytes / nanoseconds / plain numbers
         try:

@@ -748,9 +748,13 @@ struct Worker {
     int live = nxx;
     nodes++;
     B BR, NL;
-    pivot_branches(P, XP, live, BR);
-    leaf_batch(P, XP, BR, live, rlen, NL);
+    bool fresh = true;  // a node just entered: pivot + leaf batch (one call site each)
     for (;;) {
+      if (fresh) {
+        pivot_branches(P, XP, live, BR);
+        leaf_batch(P, XP, BR, live, rlen, NL);
+        fresh = false;
+      }
       const int v = first(NL);
       if (v < 0) {
         if (depth == 0) break;
@@ -820,8 +824,7 @@ struct Worker {
       rlen++;
       nodes++;
       __syncwarp();
-      pivot_branches(P, XP, live, BR);
-      leaf_batch(P, XP, BR, live, rlen, NL);
+      fresh = true;
     }
   }
 

@@ -169,43 +169,48 @@ __global__ void k_split(const int64_t* __restrict__ ro, const int32_t* __restric
 // ---- persistent parallel peel: the whole bucket-peeling loop in ONE
 // launch (software grid barrier; every CTA co-resident), no host round trip
 // per round.  Peel level k removes, round by round, every live vertex whose
-// current degree is <= k, ranking each round's removals by vertex id (so the
-// order is deterministic and identical to a round-synchronous bucket peel).
+// current degree is <= k; the position of a vertex is its (round, id) rank,
+// so the order is deterministic -- identical to a round-synchronous bucket
+// peel that ranks each round by id -- although nothing inside a round is
+// ordered: the kernel only records each vertex's round, and one radix sort of
+// (round, id) keys afterwards yields the positions.
 //
-//  * FULL round (a level's first round, or a large one): every CTA scans its
-//    chunk of the alive list (ascending ids) for live vertices with
-//    deg <= k, counts them (and the minimum live degree), grid sync, ranks
-//    them by a grid-wide prefix and compacts the survivors.
-//  * INCREMENTAL round: after a productive round the next round's removals
-//    are exactly the vertices whose degree just crossed k+1 -> k; the
-//    decrement phase appends them to a crossing list (atomics, unordered)
-//    and CTA 0 sorts it by id (block radix sort, <= PEEL_SORT_MAX) -- no scan
-//    of the alive list at all.  Larger crossing sets fall back to FULL.
+//  * FULL round (a level's first round): the CTAs scan the alive list; live
+//    vertices with deg <= k join the frontier (atomics, any order), the rest
+//    are compacted into the other alive buffer and give the minimum live
+//    degree (an empty frontier raises k to max(k + 1, that minimum)).
+//  * INCREMENTAL round: the frontier is exactly the vertices whose degree
+//    crossed k+1 -> k during the previous decrement; they were claimed right
+//    there (the unique atomicSub that returned k+1), so the round is just the
+//    decrement phase plus ONE grid barrier.
 //  * decrement: CTA-cooperative tiles of PEEL_TILE frontier vertices, their
 //    adjacency flattened over all threads (block scan of degrees + binary
 //    search for the owner), so a hub does not serialise one warp.
-// Two grid barriers per incremental round, three per full round.
 constexpr int PEEL_THREADS = 512;
-constexpr int PEEL_ITEMS = 8;
-constexpr int PEEL_SORT_MAX = PEEL_THREADS * PEEL_ITEMS;
 constexpr int PEEL_TILE = 256;
 
-struct PeelCounters {
-  int64_t take[2];
-  int32_t mindeg[2];
-  int64_t live[2];
+struct PeelShared {
+  unsigned int bar_count;
+  unsigned int bar_gen;
+  unsigned int fcount[2];   // frontier sizes, by round parity
+  unsigned int acount;      // survivors of the current full scan
+  int mindeg;               // their minimum degree
+  int pad[2];
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsigned int* gen,
-                                             unsigned int nblocks) {
+// Grid barrier; the last CTA to arrive runs `reset` (all others are waiting).
+template <typename F>
+__device__ __forceinline__ void grid_barrier(PeelShared* sh, unsigned int nblocks, F reset) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    volatile unsigned int* gen = &sh->bar_gen;
     const unsigned int g = *gen;
     __threadfence();
-    if (atomicAdd(count, 1u) == nblocks - 1) {
-      *count = 0;
+    if (atomicAdd(&sh->bar_count, 1u) == nblocks - 1) {
+      reset();
+      sh->bar_count = 0;
       __threadfence();
-      atomicAdd((unsigned int*)gen, 1u);
+      atomicAdd(&sh->bar_gen, 1u);
     } else {
       while (*gen == g) {
       }
@@ -218,225 +223,93 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, volatile unsig
 __global__ void __launch_bounds__(PEEL_THREADS)
 k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                   int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
-                  int32_t* __restrict__ frontier, int32_t* __restrict__ cross,
-                  uint8_t* __restrict__ removed, int64_t* __restrict__ pos,
-                  PeelCounters* __restrict__ blk, unsigned int* bar,
-                  int64_t* __restrict__ out_degeneracy) {
-  typedef cub::BlockReduce<int64_t, PEEL_THREADS> BRs;
-  typedef cub::BlockReduce<int32_t, PEEL_THREADS> BRm;
+                  int32_t* __restrict__ front, uint8_t* __restrict__ removed,
+                  uint64_t* __restrict__ key, PeelShared* sh, int64_t* __restrict__ out_degeneracy) {
   typedef cub::BlockScan<int32_t, PEEL_THREADS> BS;
-  typedef cub::BlockRadixSort<int32_t, PEEL_THREADS, PEEL_ITEMS> BSort;
-  typedef cub::BlockRadixSort<int32_t, PEEL_THREADS, 1> BSort1;
-  __shared__ union {
-    typename BRs::TempStorage rs;
-    typename BRm::TempStorage rm;
-    typename BS::TempStorage sc;
-    typename BSort::TempStorage so;
-    typename BSort1::TempStorage so1;
-  } tmp;
-  __shared__ int64_t s_nf, s_prefix, s_live, s_live_prefix;
-  __shared__ int32_t s_min;
+  __shared__ typename BS::TempStorage scan_tmp;
   __shared__ int64_t s_start[PEEL_TILE];
-  __shared__ int32_t s_off[PEEL_TILE + 1];
+  __shared__ int32_t s_off[PEEL_TILE];
   const unsigned int G = gridDim.x;
   const int tid = threadIdx.x;
-  unsigned int* bar_count = bar;
-  volatile unsigned int* bar_gen = bar + 1;
-  unsigned int* ncross = bar + 2;  // [2], by parity
-  const int id_bits = n > 1 ? 32 - __clz((int)(n - 1)) : 1;
+  const int64_t gtid = (int64_t)blockIdx.x * PEEL_THREADS + tid;
+  const int64_t gstride = (int64_t)G * PEEL_THREADS;
+  auto nothing = [] {};
 
-  for (int64_t v = blockIdx.x * (int64_t)PEEL_THREADS + tid; v < n; v += (int64_t)G * PEEL_THREADS) {
+  for (int64_t v = gtid; v < n; v += gstride) {
     deg[v] = (int32_t)(ro[v + 1] - ro[v]);
     alive_a[v] = (int32_t)v;
     removed[v] = 0;
   }
-  grid_barrier(bar_count, bar_gen, G);
+  grid_barrier(sh, G, nothing);
 
   int32_t* alive = alive_a;
   int32_t* alive2 = alive_b;
-  int64_t na = n;       // alive-list length (may hold removed entries after incremental rounds)
-  int64_t left = n;     // vertices not yet ranked
-  int64_t base = 0;
+  int64_t na = n, left = n;
   int32_t k = 0, deg_max = 0;
-  int parity = 0;
-  bool incremental = false;
+  int64_t r = 0;  // round
+  bool full = true;
   while (left > 0) {
+    int32_t* fr = front + (size_t)(r & 1) * n;  // this round's frontier
     int64_t nf;
-    if (incremental) {
-      nf = (int64_t)*(volatile unsigned int*)&ncross[parity];
-      if (nf == 0) {  // the level is exhausted
-        k += 1;
-        incremental = false;
-        continue;
-      }
-      if (nf > PEEL_SORT_MAX) {
-        incremental = false;  // rank by a FULL scan instead (same set, same order)
-        continue;
-      }
-      if (k > deg_max) deg_max = k;
-      if (blockIdx.x == 0) {
-        const int32_t* cl = cross + (size_t)parity * n;
-        if (nf == 1) {
-          if (tid == 0) {
-            const int32_t v = __ldcg(&cl[0]);
-            frontier[0] = v;
-            pos[v] = base;
-            removed[v] = 1;
-          }
-        } else if (nf <= PEEL_THREADS) {
-          // ids are < n <= 2^id_bits: sort only those bits (fewer passes);
-          // the stable sort keeps the all-ones padding after real ids
-          const int32_t pad = (int32_t)((1u << id_bits) - 1u);
-          int32_t key[1] = {tid < nf ? __ldcg(&cl[tid]) : pad};
-          BSort1(tmp.so1).Sort(key, 0, id_bits);
-          if (tid < nf) {
-            frontier[tid] = key[0];
-            pos[key[0]] = base + tid;
-            removed[key[0]] = 1;
-          }
+    if (full) {
+      for (int64_t i = gtid; i < na; i += gstride) {
+        const int32_t v = __ldcg(&alive[i]);
+        if (__ldcg(&removed[v])) continue;  // claimed as a crosser earlier
+        const int32_t d = __ldcg(&deg[v]);
+        if (d <= k) {
+          removed[v] = 1;
+          key[v] = ((uint64_t)r << 32) | (uint32_t)v;
+          fr[atomicAdd(&sh->fcount[r & 1], 1u)] = v;
         } else {
-          int32_t keys[PEEL_ITEMS];
-#pragma unroll
-          for (int i = 0; i < PEEL_ITEMS; ++i) {
-            const int idx = tid * PEEL_ITEMS + i;
-            keys[i] = idx < nf ? __ldcg(&cl[idx]) : 0x7fffffff;
-          }
-          BSort(tmp.so).Sort(keys);
-#pragma unroll
-          for (int i = 0; i < PEEL_ITEMS; ++i) {
-            const int idx = tid * PEEL_ITEMS + i;
-            if (idx < nf) {
-              const int32_t v = keys[i];
-              frontier[idx] = v;
-              pos[v] = base + idx;
-              removed[v] = 1;
-            }
-          }
+          alive2[atomicAdd(&sh->acount, 1u)] = v;
+          atomicMin(&sh->mindeg, d);
         }
-        if (tid == 0) ncross[parity ^ 1] = 0;
+      }
+      grid_barrier(sh, G, nothing);
+      nf = *(volatile unsigned int*)&sh->fcount[r & 1];
+      na = *(volatile unsigned int*)&sh->acount;
+      const int32_t mn = *(volatile int*)&sh->mindeg;
+      int32_t* t = alive;
+      alive = alive2;
+      alive2 = t;
+      if (nf == 0) {  // nothing at this level: jump to the next populated one
+        k = max(k + 1, mn);
+        grid_barrier(sh, G, [sh] {
+          sh->acount = 0;
+          sh->mindeg = 0x7fffffff;
+        });
+        continue;
       }
     } else {
-      // FULL: count live takes, live vertices and the minimum live degree
-      const int64_t chunk = (na + G - 1) / G;
-      const int64_t c0 = min((int64_t)blockIdx.x * chunk, na);
-      const int64_t c1 = min(c0 + chunk, na);
-      int64_t t = 0, lv = 0;
-      int32_t mn = 0x7fffffff;
-      for (int64_t i = c0 + tid; i < c1; i += PEEL_THREADS) {
-        const int32_t v = __ldcg(&alive[i]);
-        if (!__ldcg(&removed[v])) {
-          const int32_t d = __ldcg(&deg[v]);
-          t += (d <= k);
-          lv += 1;
-          mn = min(mn, d);
-        }
-      }
-      t = BRs(tmp.rs).Sum(t);
-      __syncthreads();
-      lv = BRs(tmp.rs).Sum(lv);
-      __syncthreads();
-      mn = BRm(tmp.rm).Reduce(mn, cub::Min());
-      if (tid == 0) {
-        blk[blockIdx.x].take[parity] = t;
-        blk[blockIdx.x].live[parity] = lv;
-        blk[blockIdx.x].mindeg[parity] = mn;
-      }
-      grid_barrier(bar_count, bar_gen, G);
-      int64_t tot = 0, pre = 0, ltot = 0, lpre = 0;
-      int32_t gmin = 0x7fffffff;
-      for (unsigned int b = tid; b < G; b += PEEL_THREADS) {
-        const int64_t tb = __ldcg(&blk[b].take[parity]);
-        const int64_t lb = __ldcg(&blk[b].live[parity]);
-        tot += tb;
-        ltot += lb;
-        if (b < blockIdx.x) {
-          pre += tb;
-          lpre += lb;
-        }
-        gmin = min(gmin, __ldcg(&blk[b].mindeg[parity]));
-      }
-      __syncthreads();
-      tot = BRs(tmp.rs).Sum(tot);
-      __syncthreads();
-      if (tid == 0) s_nf = tot;
-      __syncthreads();
-      pre = BRs(tmp.rs).Sum(pre);
-      __syncthreads();
-      if (tid == 0) s_prefix = pre;
-      __syncthreads();
-      lpre = BRs(tmp.rs).Sum(lpre);
-      __syncthreads();
-      if (tid == 0) s_live_prefix = lpre;
-      __syncthreads();
-      ltot = BRs(tmp.rs).Sum(ltot);
-      __syncthreads();
-      if (tid == 0) s_live = ltot;
-      __syncthreads();
-      gmin = BRm(tmp.rm).Reduce(gmin, cub::Min());
-      if (tid == 0) s_min = gmin;
-      __syncthreads();
-      nf = s_nf;
-      parity ^= 1;
-      if (nf == 0) {
-        k = max(k + 1, s_min);
+      nf = *(volatile unsigned int*)&sh->fcount[r & 1];
+      if (nf == 0) {  // the level is exhausted
+        k += 1;
+        full = true;
+        // nobody may start the full scan (which appends to this counter)
+        // before every CTA has read it
+        grid_barrier(sh, G, nothing);
         continue;
       }
-      if (k > deg_max) deg_max = k;
-      // rank the takes in alive (= id) order; compact the survivors
-      int64_t run_take = s_prefix;           // takes before this tile, grid-wide
-      int64_t run_live = s_live_prefix;      // live entries before this tile, grid-wide
-      for (int64_t tile = c0; tile < c1; tile += PEEL_THREADS) {
-        const int64_t i = tile + tid;
-        int32_t v = 0, isl = 0, flag = 0;
-        if (i < c1) {
-          v = __ldcg(&alive[i]);
-          isl = !__ldcg(&removed[v]);
-          flag = isl && __ldcg(&deg[v]) <= k;
-        }
-        // pack (take, live) into one scan: live < 2^16 per tile
-        int32_t excl = 0, tot_packed = 0;
-        BS(tmp.sc).ExclusiveSum(flag | (isl << 16), excl, tot_packed);
-        __syncthreads();
-        const int32_t ex_take = excl & 0xffff, ex_live = excl >> 16;
-        if (i < c1 && isl) {
-          if (flag) {
-            const int64_t r = run_take + ex_take;
-            pos[v] = base + r;
-            frontier[r] = v;
-            removed[v] = 1;
-          } else {
-            // survivors before v = live before v - takes before v
-            alive2[(run_live + ex_live) - (run_take + ex_take)] = v;
-          }
-        }
-        run_take += tot_packed & 0xffff;
-        run_live += tot_packed >> 16;
-      }
-      if (blockIdx.x == 0 && tid == 0) ncross[parity] = 0;
-      int32_t* t2 = alive;
-      alive = alive2;
-      alive2 = t2;
-      na = s_live - nf;
     }
-    grid_barrier(bar_count, bar_gen, G);
-    // decrement: CTA-cooperative tiles of the frontier; crossers k+1 -> k
-    // go to the crossing list of the next round (parity after the flip)
-    const int np = incremental ? (parity ^ 1) : parity;
+    if (k > deg_max) deg_max = k;
+    // decrement the live neighbours of the frontier; the unique k+1 -> k
+    // crossing claims the vertex for round r + 1
+    int32_t* nx = front + (size_t)((r + 1) & 1) * n;
+    const uint64_t next_tag = (uint64_t)(r + 1) << 32;
     for (int64_t tile = (int64_t)blockIdx.x * PEEL_TILE; tile < nf; tile += (int64_t)G * PEEL_TILE) {
       int32_t d = 0;
       int64_t st = 0;
       if (tid < PEEL_TILE && tile + tid < nf) {
-        const int32_t v = __ldcg(&frontier[tile + tid]);
+        const int32_t v = __ldcg(&fr[tile + tid]);
         st = ro[v];
         d = (int32_t)(ro[v + 1] - st);
       }
       int32_t off = 0, total = 0;
-      BS(tmp.sc).ExclusiveSum(d, off, total);
+      BS(scan_tmp).ExclusiveSum(d, off, total);
       if (tid < PEEL_TILE) {
         s_start[tid] = st;
         s_off[tid] = off;
       }
-      if (tid == 0) s_off[PEEL_TILE] = total;
       __syncthreads();
       for (int32_t e = tid; e < total; e += PEEL_THREADS) {
         int lo = 0, hi = PEEL_TILE;  // last owner with s_off[owner] <= e
@@ -446,22 +319,35 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         }
         const int32_t u = col[s_start[lo] + (e - s_off[lo])];
         if (!__ldcg(&removed[u])) {
-          const int32_t old = atomicSub(&deg[u], 1);
-          if (old == k + 1) {
-            const unsigned int slot = atomicAdd(&ncross[np], 1u);
-            cross[(size_t)np * n + slot] = u;
+          if (atomicSub(&deg[u], 1) == k + 1) {
+            removed[u] = 1;
+            key[u] = next_tag | (uint32_t)u;
+            nx[atomicAdd(&sh->fcount[(r + 1) & 1], 1u)] = u;
           }
         }
       }
       __syncthreads();
     }
-    grid_barrier(bar_count, bar_gen, G);
-    if (incremental) parity ^= 1;
-    base += nf;
+    // every CTA has read fcount[r & 1]: it becomes round r + 2's counter
+    const int par = (int)(r & 1);
+    grid_barrier(sh, G, [sh, par] {
+      sh->fcount[par] = 0;
+      sh->acount = 0;
+      sh->mindeg = 0x7fffffff;
+    });
     left -= nf;
-    incremental = true;
+    r += 1;
+    full = false;
   }
   if (blockIdx.x == 0 && tid == 0) *out_degeneracy = deg_max;
+}
+
+// positions from the sorted (round, id) keys
+__global__ void k_peel_positions(const uint64_t* __restrict__ sorted, int64_t n,
+                                 int64_t* __restrict__ pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pos[(uint32_t)sorted[i]] = i;
 }
 
 // ---- exact order (reference tie-break): single CTA, min-segment-tree over
@@ -588,7 +474,8 @@ int csr_from_sorted_keys(mce_graph* g, uint64_t* keys, int64_t nnz, int b, cudaS
   return mce_graph_build_split(g, s);
 }
 
-// Bucket peeling in one persistent launch; positions to d_pos (device).
+// Bucket peeling in one persistent launch + one (round, id) sort; positions
+// to d_pos (device).
 int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaStream_t s) {
   const int64_t n = g->n;
   int dev = 0, sms = 0, per_sm = 0;
@@ -602,27 +489,32 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaS
   }
   // every CTA must be co-resident (software grid barrier)
   int64_t grid = std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, (n + 2047) / 2048));
-  int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *frontier = nullptr;
-  int32_t* cross = nullptr;
+  int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *front = nullptr;
   uint8_t* removed = nullptr;
-  PeelCounters* blk = nullptr;
-  unsigned int* bar = nullptr;  // barrier count, generation, crossing counters [2]
+  uint64_t* key = nullptr;
+  PeelShared* sh = nullptr;
   int64_t* d_deg = nullptr;
   if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
-      dev_alloc(&frontier, n, s) || dev_alloc(&cross, 2 * n, s) || dev_alloc(&removed, n, s) ||
-      dev_alloc(&blk, grid, s) || dev_alloc(&bar, 4, s) || dev_alloc(&d_deg, 1, s))
+      dev_alloc(&front, 2 * n, s) || dev_alloc(&removed, n, s) || dev_alloc(&key, n, s) ||
+      dev_alloc(&sh, 1, s) || dev_alloc(&d_deg, 1, s))
     return -1;
-  MCE_CHECK(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned int), s));
+  PeelShared init{};
+  init.mindeg = 0x7fffffff;
+  MCE_CHECK(cudaMemcpyAsync(sh, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   k_peel_persistent<<<(int)grid, PEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2,
-                                                      frontier, cross, removed, d_pos, blk, bar,
-                                                      d_deg);
+                                                      front, removed, key, sh, d_deg);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  // rounds < n, ids < 2^31: sort the (round, id) keys over the bits they use
+  const int rb = bits_for(std::max<int64_t>(n, 2));
+  if (sort_keys(&key, n, 32 + rb, s)) return -1;
+  k_peel_positions<<<grid_for(n), 256, 0, s>>>(key, n, d_pos);
+  mce_count_launch();
+  MCE_CHECK(cudaGetLastError());
   MCE_CHECK(cudaStreamSynchronize(s));
-  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(frontier, s);
-  dev_free(cross, s); dev_free(removed, s); dev_free(blk, s); dev_free(bar, s);
-  dev_free(d_deg, s);
+  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(front, s);
+  dev_free(removed, s); dev_free(key, s); dev_free(sh, s); dev_free(d_deg, s);
   return 0;
 }
 

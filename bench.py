@@ -61,6 +61,7 @@ def parse_args():
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     p.add_argument("--shard", default="static", choices=["static", "steal"],
                    help="N>1: static interleave, or static + work-stealing chunks")
     return p.parse_args()
@@ -74,8 +75,9 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int = 0):
+    def __init__(self, index: int = 0, enabled: bool = True):
         self.index = index
+        self.enabled = enabled
         self.samples: list[list[str]] = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._loop, daemon=True)
@@ -94,12 +96,14 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
-        self._t.start()
+        if self.enabled:
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self.enabled:
+            self._t.join(timeout=10)
 
     def summary(self) -> dict:
         def num(x):
@@ -252,7 +256,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # 2x the 126 MB L2
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local, enabled=not args.no_clocks) as clocks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()

@@ -349,7 +349,33 @@ struct Worker {
     return contains_range(a.col, a.split[x], a.ro[x + 1], gv);
   }
 
-  __device__ bool xx_any_adjacent(int v, int32_t gv, int live) const {
+  // Is any live X_X member adjacent to branch vertex v (global gv)?  Without
+  // X rows, either test each live member x for gv in N+(x), or -- when the
+  // live prefix is known ascending (`sorted`: the root's tokens and every
+  // kept part cut from an ascending prefix) and gv has fewer earlier
+  // neighbours than there are live members -- look each y in N-(gv) up in
+  // the live prefix by binary search.
+  __device__ bool xx_any_adjacent(int v, int32_t gv, int live, bool sorted = false) const {
+    if (!XROWS && sorted) {
+      const int64_t nb = a.ro[gv], ne = a.split[gv];
+      if (ne - nb < live) {
+        for (int64_t base = nb; base < ne; base += 32) {
+          const int64_t e = base + lane;
+          bool hit = false;
+          if (e < ne) {
+            const int32_t y = a.col[e];
+            int lo = 0, hi = live;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (root_x[xx[mid]] < y) lo = mid + 1; else hi = mid;
+            }
+            hit = lo < live && root_x[xx[lo]] == y;
+          }
+          if (__any_sync(FULLMASK, hit)) return true;
+        }
+        return false;
+      }
+    }
     for (int base = 0; base < live; base += 32) {
       int i = base + lane;
       bool hit = (i < live) && xx_adjacent(xx[i], v, gv);
@@ -488,7 +514,8 @@ struct Worker {
   // are decided in one lane-per-candidate pass: node count += #leaves, the
   // maximal ones (X_v & N(v) empty, X_v = X_P plus the earlier branches, and
   // no live X_X neighbour) are reported together.  Returns BR minus leaves.
-  __device__ void leaf_batch(const B& P, const B& XP, const B& BR, int live, int rlen, B& NL) {
+  __device__ void leaf_batch(const B& P, const B& XP, const B& BR, int live, int rlen, B& NL,
+                             bool xsorted) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       if (valid(k, lane)) {
@@ -546,7 +573,7 @@ struct Worker {
             for (unsigned t = xm; t; t &= t - 1) {
               const int b = __ffs(t) - 1;
               const int v = (w << 5) + b;
-              if (xx_any_adjacent(v, plist[v], live)) xm &= ~(1u << b);
+              if (xx_any_adjacent(v, plist[v], live, xsorted)) xm &= ~(1u << b);
             }
           }
         }
@@ -731,7 +758,7 @@ struct Worker {
   // Leaves are settled per node by leaf_batch; the loop walks the non-leaf
   // branches in the reference's order, applying the P -> X_P moves of the
   // leaf branches that precede each one.
-  __device__ void traverse(B P, B XP, int nxx, int rlen) {
+  __device__ void traverse(B P, B XP, int nxx, int rlen, bool root_sorted) {
     uint64_t hs = 0;
     for (int i = 0; i < rlen; ++i) hs += a.vhash[rpath[i]];
     if (!any(P)) {  // scheduler.py:300-304
@@ -749,10 +776,12 @@ struct Worker {
     nodes++;
     B BR, NL;
     bool fresh = true;  // a node just entered: pivot + leaf batch (one call site each)
+    // bit d: the live X_X prefix at depth d is ascending (see xx_any_adjacent)
+    unsigned long long xsorted = root_sorted ? 1ull : 0ull;
     for (;;) {
       if (fresh) {
         pivot_branches(P, XP, live, BR);
-        leaf_batch(P, XP, BR, live, rlen, NL);
+        leaf_batch(P, XP, BR, live, rlen, NL, depth < 64 && ((xsorted >> depth) & 1ull));
         fresh = false;
       }
       const int v = first(NL);
@@ -807,6 +836,13 @@ struct Worker {
         continue;
       }
       const int kept = partition(v, gv, live);
+      if (depth < 63) {  // the kept part inherits the order; the parent's prefix is permuted
+        const unsigned long long bit = (xsorted >> depth) & 1ull;
+        xsorted &= ~(3ull << depth);
+        xsorted |= bit << (depth + 1);
+      } else {
+        xsorted = 0;
+      }
       push(depth, P, XP, BR, NL);
       if (any(NL)) below++;
       depth++;
@@ -844,7 +880,7 @@ struct Worker {
     }
     for (int t = lane; t < nx; t += 32) xx[t] = t;
     __syncwarp();
-    traverse(P, XP, nx, nr);
+    traverse(P, XP, nx, nr, true);
   }
 
   __device__ void run_donated() {
@@ -872,7 +908,7 @@ struct Worker {
       rpath[1] = keep1;
     }
     __syncwarp();
-    traverse(P, XP, nxx, rlen);
+    traverse(P, XP, nxx, rlen, false);
   }
 };
 

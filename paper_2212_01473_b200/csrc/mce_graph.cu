@@ -176,26 +176,25 @@ __global__ void k_split(const int64_t* __restrict__ ro, const int32_t* __restric
 // (round, id) keys afterwards yields the positions.
 //
 //  * FULL round (a level's first round): the CTAs scan the alive list; live
-//    vertices with deg <= k join the frontier (atomics, any order), the rest
-//    are compacted into the other alive buffer and give the minimum live
-//    degree (an empty frontier raises k to max(k + 1, that minimum)).
+//    vertices with deg <= k join the frontier, the rest are compacted into the
+//    other alive buffer and give the minimum live degree (an empty frontier
+//    raises k to max(k + 1, that minimum)).
 //  * INCREMENTAL round: the frontier is exactly the vertices whose degree
 //    crossed k+1 -> k during the previous decrement; they were claimed right
 //    there (the unique atomicSub that returned k+1), so the round is just the
 //    decrement phase plus ONE grid barrier.
-//  * decrement: CTA-cooperative tiles of PEEL_TILE frontier vertices, their
-//    adjacency flattened over all threads (block scan of degrees + binary
-//    search for the owner), so a hub does not serialise one warp.
+//  * decrement work list: a frontier vertex enters as ceil(deg/32) chunk
+//    descriptors (vertex, chunk); warps take descriptors grid-wide, one lane
+//    per edge, so a hub's adjacency is spread over many warps.
 constexpr int PEEL_THREADS = 512;
-constexpr int PEEL_TILE = 256;
 
 struct PeelShared {
   unsigned int bar_count;
   unsigned int bar_gen;
-  unsigned int fcount[2];   // frontier sizes, by round parity
+  unsigned int fcount[2];   // frontier vertices, by round parity
+  unsigned int ccount[2];   // frontier chunk descriptors, by round parity
   unsigned int acount;      // survivors of the current full scan
   int mindeg;               // their minimum degree
-  int pad[2];
 };
 
 // Grid barrier; the last CTA to arrive runs `reset` (all others are waiting).
@@ -220,19 +219,31 @@ __device__ __forceinline__ void grid_barrier(PeelShared* sh, unsigned int nblock
   __syncthreads();
 }
 
+// frontier vertex v of the round with parity p: ceil(deg/32) descriptors
+__device__ __forceinline__ void peel_enqueue(const int64_t* __restrict__ ro, int32_t v, int p,
+                                             uint64_t* __restrict__ chunks, int64_t cap,
+                                             PeelShared* sh) {
+  atomicAdd(&sh->fcount[p], 1u);
+  const unsigned nch = (unsigned)((ro[v + 1] - ro[v] + 31) >> 5);
+  if (nch == 0) return;
+  const unsigned base = atomicAdd(&sh->ccount[p], nch);
+  uint64_t* out = chunks + (size_t)p * cap + base;
+  for (unsigned j = 0; j < nch; ++j) out[j] = ((uint64_t)(uint32_t)v << 32) | j;
+}
+
 __global__ void __launch_bounds__(PEEL_THREADS)
 k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                   int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
-                  int32_t* __restrict__ front, uint8_t* __restrict__ removed,
-                  uint64_t* __restrict__ key, PeelShared* sh, int64_t* __restrict__ out_degeneracy) {
-  typedef cub::BlockScan<int32_t, PEEL_THREADS> BS;
-  __shared__ typename BS::TempStorage scan_tmp;
-  __shared__ int64_t s_start[PEEL_TILE];
-  __shared__ int32_t s_off[PEEL_TILE];
+                  uint64_t* __restrict__ chunks, int64_t chunk_cap,
+                  uint8_t* __restrict__ removed, uint64_t* __restrict__ key, PeelShared* sh,
+                  int64_t* __restrict__ out_degeneracy) {
   const unsigned int G = gridDim.x;
   const int tid = threadIdx.x;
+  const int lane = tid & 31;
   const int64_t gtid = (int64_t)blockIdx.x * PEEL_THREADS + tid;
   const int64_t gstride = (int64_t)G * PEEL_THREADS;
+  const int64_t gwarp = gtid >> 5;
+  const int64_t nwarps = gstride >> 5;
   auto nothing = [] {};
 
   for (int64_t v = gtid; v < n; v += gstride) {
@@ -249,7 +260,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
   int64_t r = 0;  // round
   bool full = true;
   while (left > 0) {
-    int32_t* fr = front + (size_t)(r & 1) * n;  // this round's frontier
+    const int p = (int)(r & 1);
     int64_t nf;
     if (full) {
       for (int64_t i = gtid; i < na; i += gstride) {
@@ -259,14 +270,14 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         if (d <= k) {
           removed[v] = 1;
           key[v] = ((uint64_t)r << 32) | (uint32_t)v;
-          fr[atomicAdd(&sh->fcount[r & 1], 1u)] = v;
+          peel_enqueue(ro, v, p, chunks, chunk_cap, sh);
         } else {
           alive2[atomicAdd(&sh->acount, 1u)] = v;
           atomicMin(&sh->mindeg, d);
         }
       }
       grid_barrier(sh, G, nothing);
-      nf = *(volatile unsigned int*)&sh->fcount[r & 1];
+      nf = *(volatile unsigned int*)&sh->fcount[p];
       na = *(volatile unsigned int*)&sh->acount;
       const int32_t mn = *(volatile int*)&sh->mindeg;
       int32_t* t = alive;
@@ -281,12 +292,12 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         continue;
       }
     } else {
-      nf = *(volatile unsigned int*)&sh->fcount[r & 1];
+      nf = *(volatile unsigned int*)&sh->fcount[p];
       if (nf == 0) {  // the level is exhausted
         k += 1;
         full = true;
-        // nobody may start the full scan (which appends to this counter)
-        // before every CTA has read it
+        // nobody may start the full scan (which appends to this round's
+        // counters) before every CTA has read them
         grid_barrier(sh, G, nothing);
         continue;
       }
@@ -294,44 +305,26 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
     if (k > deg_max) deg_max = k;
     // decrement the live neighbours of the frontier; the unique k+1 -> k
     // crossing claims the vertex for round r + 1
-    int32_t* nx = front + (size_t)((r + 1) & 1) * n;
+    const int64_t nc = *(volatile unsigned int*)&sh->ccount[p];
+    const uint64_t* cl = chunks + (size_t)p * chunk_cap;
     const uint64_t next_tag = (uint64_t)(r + 1) << 32;
-    for (int64_t tile = (int64_t)blockIdx.x * PEEL_TILE; tile < nf; tile += (int64_t)G * PEEL_TILE) {
-      int32_t d = 0;
-      int64_t st = 0;
-      if (tid < PEEL_TILE && tile + tid < nf) {
-        const int32_t v = __ldcg(&fr[tile + tid]);
-        st = ro[v];
-        d = (int32_t)(ro[v + 1] - st);
-      }
-      int32_t off = 0, total = 0;
-      BS(scan_tmp).ExclusiveSum(d, off, total);
-      if (tid < PEEL_TILE) {
-        s_start[tid] = st;
-        s_off[tid] = off;
-      }
-      __syncthreads();
-      for (int32_t e = tid; e < total; e += PEEL_THREADS) {
-        int lo = 0, hi = PEEL_TILE;  // last owner with s_off[owner] <= e
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_off[mid] <= e) lo = mid; else hi = mid;
-        }
-        const int32_t u = col[s_start[lo] + (e - s_off[lo])];
-        if (!__ldcg(&removed[u])) {
-          if (atomicSub(&deg[u], 1) == k + 1) {
-            removed[u] = 1;
-            key[u] = next_tag | (uint32_t)u;
-            nx[atomicAdd(&sh->fcount[(r + 1) & 1], 1u)] = u;
-          }
+    for (int64_t c = gwarp; c < nc; c += nwarps) {
+      const uint64_t dsc = __ldcg(&cl[c]);
+      const int32_t v = (int32_t)(dsc >> 32);
+      const int64_t e = ro[v] + ((int64_t)(uint32_t)dsc << 5) + lane;
+      if (e < ro[v + 1]) {
+        const int32_t u = col[e];
+        if (!__ldcg(&removed[u]) && atomicSub(&deg[u], 1) == k + 1) {
+          removed[u] = 1;
+          key[u] = next_tag | (uint32_t)u;
+          peel_enqueue(ro, u, p ^ 1, chunks, chunk_cap, sh);
         }
       }
-      __syncthreads();
     }
-    // every CTA has read fcount[r & 1]: it becomes round r + 2's counter
-    const int par = (int)(r & 1);
-    grid_barrier(sh, G, [sh, par] {
-      sh->fcount[par] = 0;
+    // every CTA has read this round's counters: they become round r + 2's
+    grid_barrier(sh, G, [sh, p] {
+      sh->fcount[p] = 0;
+      sh->ccount[p] = 0;
       sh->acount = 0;
       sh->mindeg = 0x7fffffff;
     });
@@ -489,20 +482,24 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaS
   }
   // every CTA must be co-resident (software grid barrier)
   int64_t grid = std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, (n + 2047) / 2048));
-  int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *front = nullptr;
+  int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr;
+  uint64_t* chunks = nullptr;
   uint8_t* removed = nullptr;
   uint64_t* key = nullptr;
   PeelShared* sh = nullptr;
   int64_t* d_deg = nullptr;
+  // one round's descriptors: sum over its vertices of ceil(deg/32) <= n + 2m/32
+  const int64_t chunk_cap = n + g->nnz / 32 + 1;
   if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
-      dev_alloc(&front, 2 * n, s) || dev_alloc(&removed, n, s) || dev_alloc(&key, n, s) ||
-      dev_alloc(&sh, 1, s) || dev_alloc(&d_deg, 1, s))
+      dev_alloc(&chunks, 2 * chunk_cap, s) || dev_alloc(&removed, n, s) ||
+      dev_alloc(&key, n, s) || dev_alloc(&sh, 1, s) || dev_alloc(&d_deg, 1, s))
     return -1;
   PeelShared init{};
   init.mindeg = 0x7fffffff;
   MCE_CHECK(cudaMemcpyAsync(sh, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   k_peel_persistent<<<(int)grid, PEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2,
-                                                      front, removed, key, sh, d_deg);
+                                                      chunks, chunk_cap, removed, key, sh,
+                                                      d_deg);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -513,7 +510,7 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaS
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   MCE_CHECK(cudaStreamSynchronize(s));
-  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(front, s);
+  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(chunks, s);
   dev_free(removed, s); dev_free(key, s); dev_free(sh, s); dev_free(d_deg, s);
   return 0;
 }

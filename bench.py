@@ -68,35 +68,81 @@ def parse_args():
 
 
 class ClockSampler:
-    """Samples nvidia-smi SM clocks and throttle reasons during the timed region."""
+    """Samples SM clocks and clock-event (throttle) reasons DURING the timed
+    region through NVML in-process (every 10 ms; an nvidia-smi subprocess per
+    sample would perturb the host side of a millisecond-scale step), falling
+    back to nvidia-smi when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int = 0, enabled: bool = True):
+    def __init__(self, index: int = 0, enabled: bool = True, period: float = 0.01):
         self.index = index
         self.enabled = enabled
-        self.samples: list[list[str]] = []
+        self.period = period
+        self.samples: list[tuple[float | None, float | None, set]] = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._loop, daemon=True)
+        self._nvml = None
+
+    def _nvml_init(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self._nvml = (pynvml, h, bits)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        pynvml, h, bits = self._nvml
+        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+        mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        return sm, mx, {k for k, b in bits.items() if r & b}
+
+    def _sample_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={fields}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5)
+        row = [x.strip() for x in out.stdout.strip().split(",")]
+        if len(row) != 6:
+            return None
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        return num(row[0]), num(row[1]), {self.NAMES[i] for i in range(4)
+                                         if row[2 + i].lower() in ("active", "1")}
 
     def _loop(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                row = [x.strip() for x in out.stdout.strip().split(",")]
-                if len(row) == 6:
-                    self.samples.append(row)
+                smp = self._sample_nvml() if self._nvml else self._sample_smi()
+                if smp:
+                    self.samples.append(smp)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(self.period if self._nvml else 0.1)
 
     def __enter__(self):
         if self.enabled:
+            self._nvml_init()
+            try:  # one sample before the region starts, so short regions still get one
+                smp = self._sample_nvml() if self._nvml else self._sample_smi()
+                if smp:
+                    self.samples.append(smp)
+            except Exception:
+                pass
             self._t.start()
         return self
 
@@ -106,18 +152,13 @@ class ClockSampler:
             self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = sorted(v for v in (num(r[0]) for r in self.samples) if v is not None)
-        mx = [v for v in (num(r[1]) for r in self.samples) if v is not None]
-        reasons = sorted({self.NAMES[i] for r in self.samples for i in range(4)
-                          if r[2 + i].lower() in ("active", "1")})
+        sm = sorted(x[0] for x in self.samples if x[0] is not None)
+        mx = [x[1] for x in self.samples if x[1] is not None]
+        reasons = sorted(set().union(*[x[2] for x in self.samples])) if self.samples else []
         return {"sm_mhz": sm[len(sm) // 2] if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def measured_hbm_peak() -> tuple[float, str]:

@@ -1037,7 +1037,9 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
   __syncthreads();
   if (threadIdx.x <= TRIVIAL_RANK && s_cls[threadIdx.x])
     atomicAdd(&classes[threadIdx.x], (unsigned long long)s_cls[threadIdx.x]);
-  if (local_max) atomicMax(max_p, local_max);
+  // one atomic per warp, not per thread (a contended address serialises in L2)
+  local_max = __reduce_max_sync(FULLMASK, (unsigned)min(local_max, 0xffffffffull));
+  if ((threadIdx.x & 31) == 0 && local_max) atomicMax(max_p, local_max);
 }
 
 // Algorithmic bytes one root's induced-subgraph build must read from the CSR:

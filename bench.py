@@ -69,9 +69,11 @@ def parse_args():
 
 class ClockSampler:
     """Samples SM clocks and clock-event (throttle) reasons DURING the timed
-    region through NVML in-process (every 10 ms; an nvidia-smi subprocess per
-    sample would perturb the host side of a millisecond-scale step), falling
-    back to nvidia-smi when NVML is unavailable."""
+    region through NVML in-process, falling back to nvidia-smi.  The bench
+    calls ``sample_now()`` between timed steps (after a step's end event,
+    before the next start event): a concurrent sampler thread contends with
+    the CUDA driver calls of a millisecond-scale step and shows up as GPU
+    idle time inside the events."""
 
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
@@ -134,22 +136,23 @@ class ClockSampler:
                 pass
             self._stop.wait(self.period if self._nvml else 0.1)
 
+    def sample_now(self):
+        if not self.enabled:
+            return
+        try:
+            smp = self._sample_nvml() if self._nvml else self._sample_smi()
+            if smp:
+                self.samples.append(smp)
+        except Exception:
+            pass
+
     def __enter__(self):
         if self.enabled:
             self._nvml_init()
-            try:  # one sample before the region starts, so short regions still get one
-                smp = self._sample_nvml() if self._nvml else self._sample_smi()
-                if smp:
-                    self.samples.append(smp)
-            except Exception:
-                pass
-            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        if self.enabled:
-            self._t.join(timeout=10)
 
     def summary(self) -> dict:
         sm = sorted(x[0] for x in self.samples if x[0] is not None)
@@ -307,6 +310,7 @@ def main():
             res, tot, st = one_job(g)
             ends[i].record()
             kernel_ms += res.kernel_ms
+            clocks.sample_now()  # between the events: host time only
         torch.cuda.synchronize()
     launches = _lib.lib().mce_launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]

@@ -39,6 +39,8 @@ namespace {
 constexpr int HIST_SMEM = 128;
 constexpr int HIST_MAX = MCE_HIST_MAX;
 constexpr unsigned FULLMASK = 0xffffffffu;
+constexpr int ROOT_STRIPES = 32;  // root-claim counters (<= 32: one per lane in phase2())
+constexpr int ROOT_STRIDE = 16;   // 128 B apart
 
 // Lock-free worker list (paper §3.3, reference scheduler.py:99-165).  A parked
 // worker sets its bit in `idle_bits`; a donor claims a receiver by clearing
@@ -68,7 +70,7 @@ struct EnumArgs {
   const uint64_t* vhash;  // mix64(label(v))
   const int64_t* roots;   // l1: vertex, l2: (u << 32) | v
   int64_t num_roots;
-  unsigned long long* root_counter;
+  unsigned long long* root_counter;  // ROOT_STRIPES counters, ROOT_STRIDE apart
   int roots_mode;
   int num_workers;
   int64_t xcap;
@@ -619,12 +621,32 @@ struct Worker {
     __syncwarp();
   }
 
+  // phase 2 = every root claimed: every stripe counter past its stripe
   __device__ bool phase2() {
     if (!phase2_seen) {
-      unsigned long long c = *(volatile unsigned long long*)a.root_counter;
-      phase2_seen = c >= (unsigned long long)a.num_roots;
+      const unsigned long long c =
+          lane < ROOT_STRIPES ? *(volatile unsigned long long*)&a.root_counter[lane * ROOT_STRIDE] : 0ull;
+      const bool done = lane >= ROOT_STRIPES ||
+                        c * ROOT_STRIPES + lane >= (unsigned long long)a.num_roots;
+      phase2_seen = __all_sync(FULLMASK, done);
     }
     return phase2_seen;
+  }
+
+  // Next root (sorted heaviest first) or -1.  Roots are dealt round-robin into
+  // ROOT_STRIPES stripes, each with its own counter: a warp claims from its
+  // home stripe and moves on when it runs dry, so 10^4 warps do not
+  // serialise on one L2 atomic while the claim order stays heaviest-first.
+  __device__ int64_t claim_root(int& stripe) {
+    for (int tried = 0; tried < ROOT_STRIPES; ++tried) {
+      unsigned long long idx = 0;
+      if (lane == 0) idx = atomicAdd(&a.root_counter[stripe * ROOT_STRIDE], 1ull);
+      idx = __shfl_sync(FULLMASK, idx, 0);
+      const unsigned long long r = idx * ROOT_STRIPES + stripe;
+      if (r < (unsigned long long)a.num_roots) return (int64_t)r;
+      stripe = (stripe + 1) % ROOT_STRIPES;
+    }
+    return -1;
   }
 
   // donate the branch (v, childP, childXP) to an idle worker (scheduler.py:417-438)
@@ -942,11 +964,10 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
     Worker<W, PIVOT_XX, XROWS, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
                                   s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + 3 * warp * SPW,
                                   s_hist);
+    int stripe = wid % ROOT_STRIPES;
     for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-273)
-      unsigned long long idx = 0;
-      if (lane == 0) idx = atomicAdd(a.root_counter, 1ull);
-      idx = __shfl_sync(FULLMASK, idx, 0);
-      if (idx >= (unsigned long long)a.num_roots) break;
+      const int64_t idx = wk.claim_root(stripe);
+      if (idx < 0) break;
       wk.roots_claimed++;
       wk.run_root(a.roots[idx]);
     }
@@ -1204,7 +1225,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
       get(&args.mbox, (size_t)workers) || get(&args.mbits, (size_t)workers * 2 * W) ||
       get(&args.idle_bits, (size_t)(workers + 31) / 32) ||
       get(&args.wl_wake, (size_t)workers) || get(&args.wl, 1) ||
-      get(&args.root_counter, 1))
+      get(&args.root_counter, ROOT_STRIPES * ROOT_STRIDE))
     return -1;
   args.xrows = nullptr;
   args.xlist = nullptr;
@@ -1219,7 +1240,8 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   MCE_CHECK(cudaMemsetAsync(args.wl_wake, 0, sizeof(int) * workers, s));
   MCE_CHECK(cudaMemsetAsync(args.idle_bits, 0, sizeof(unsigned) * ((workers + 31) / 32), s));
   MCE_CHECK(cudaMemsetAsync(args.mbox, 0, sizeof(Mailbox) * workers, s));
-  MCE_CHECK(cudaMemsetAsync(args.root_counter, 0, sizeof(unsigned long long), s));
+  MCE_CHECK(cudaMemsetAsync(args.root_counter, 0,
+                            sizeof(unsigned long long) * ROOT_STRIPES * ROOT_STRIDE, s));
   const int grid = (int)((workers + WARPS - 1) / WARPS);
   MCE_CHECK(cudaEventRecord(ev[0], s));
   kern<<<grid, WARPS * 32, smem, s>>>(args);

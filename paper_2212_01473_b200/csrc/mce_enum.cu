@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -90,6 +91,7 @@ struct EnumArgs {
   unsigned long long* g_acc;   // 0 cliques, 1 hash, 2 nodes, 3 donations, 4 max size
   unsigned long long* g_hist;  // HIST_MAX
   long long* w_metrics;        // per worker: nodes, roots, donations made, received
+  long long* root_cycles;      // diagnostics (MCE_PROFILE_ROOTS): SM cycles per claimed root
   int64_t* collect;
   int64_t collect_cap;
   unsigned long long* collect_len;
@@ -969,7 +971,9 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
       const int64_t idx = wk.claim_root(stripe);
       if (idx < 0) break;
       wk.roots_claimed++;
+      const long long t0 = a.root_cycles ? clock64() : 0;
       wk.run_root(a.roots[idx]);
+      if (a.root_cycles && lane == 0) a.root_cycles[idx] = clock64() - t0;
     }
     if (a.worker_list_on) {  // phase 2: park, receive donated branches
       while (wk.park()) {
@@ -1395,6 +1399,14 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     MCE_CHECK(cudaMemcpyAsync(hc, cls, sizeof(hc), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
     const int64_t* sorted_roots = dv.Current();
+    // diagnostics: MCE_PROFILE_ROOTS=<file> dumps (root, W, cycles) per root
+    const char* prof_path = getenv("MCE_PROFILE_ROOTS");
+    long long* prof_cycles = nullptr;
+    if (prof_path && get(&prof_cycles, count)) {
+      cleanup();
+      return -1;
+    }
+    if (prof_cycles) MCE_CHECK(cudaMemsetAsync(prof_cycles, 0, sizeof(long long) * count, s));
     const int64_t cap_limit = std::min<int64_t>(
         cfg->capacity_bits > 0 ? cfg->capacity_bits : MAX_CAPACITY_BITS, MAX_CAPACITY_BITS);
     const int64_t max_p = (int64_t)hc[MAXP_SLOT];
@@ -1446,6 +1458,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.g_acc = acc;
       args.g_hist = hist;
       args.w_metrics = wmet;
+      args.root_cycles = prof_cycles ? prof_cycles + cp.begin : nullptr;
       args.collect = d_collect;
       args.collect_cap = cfg->collect_cap;
       args.collect_len = collect_len;
@@ -1471,6 +1484,23 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       wcap = std::max<int64_t>(wcap, req > 0 ? req : metric_slots);
     }
     max_workers_slots = std::max<int64_t>(workers_used, 1);
+    if (prof_cycles) {
+      std::vector<long long> cyc(count);
+      std::vector<int64_t> rts(count);
+      MCE_CHECK(cudaMemcpyAsync(cyc.data(), prof_cycles, sizeof(long long) * count,
+                                cudaMemcpyDeviceToHost, s));
+      MCE_CHECK(cudaMemcpyAsync(rts.data(), sorted_roots, sizeof(int64_t) * count,
+                                cudaMemcpyDeviceToHost, s));
+      MCE_CHECK(cudaStreamSynchronize(s));
+      if (FILE* f = fopen(prof_path, "wb")) {
+        for (const ClassPlan& cp : plan)
+          for (int64_t i = cp.begin; i < cp.begin + cp.count; ++i) {
+            const int64_t rec[3] = {rts[i], (int64_t)cp.W, (int64_t)cyc[i]};
+            fwrite(rec, sizeof(rec), 1, f);
+          }
+        fclose(f);
+      }
+    }
     if (trivial_count > 0) {
       k_trivial_roots<<<grid_for(trivial_count), 256, 0, s>>>(
           sorted_roots + trivial_begin, trivial_count, g->ro, g->split, vhash, acc, hist,

@@ -85,6 +85,28 @@ __global__ void k_edge_keys(const int64_t* __restrict__ edges, int64_t m, int b,
   if (__syncthreads_or(oob) && threadIdx.x == 0) atomicExch(bad, 1);
 }
 
+// both directed keys of every input pair; loops -> all-ones (dropped later)
+__global__ void k_edge_keys_both(const int64_t* __restrict__ edges, int64_t m, int b, int64_t n,
+                                 uint64_t* __restrict__ keys, int* __restrict__ bad) {
+  bool oob = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = edges[2 * i], c = edges[2 * i + 1];
+    oob |= (a < 0) | (c < 0) | (a >= n) | (c >= n);
+    const bool loop = a == c;
+    keys[2 * i] = loop ? ~0ull : (((uint64_t)a << b) | (uint64_t)c);
+    keys[2 * i + 1] = loop ? ~0ull : (((uint64_t)c << b) | (uint64_t)a);
+  }
+  if (__syncthreads_or(oob) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+// cnt[2] = 1 when the last unique key is the (sorted-last) loop sentinel
+__global__ void k_last_is_loop(const uint64_t* __restrict__ uniq, int64_t* cnt, int bits) {
+  const int64_t u = cnt[0];
+  const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+  cnt[2] = (u > 0 && (uniq[u - 1] & mask) == mask) ? 1 : 0;
+}
+
 struct NotAllOnes {
   __host__ __device__ bool operator()(const uint64_t& k) const { return k != ~0ull; }
 };
@@ -191,8 +213,9 @@ constexpr int PEEL_THREADS = 512;
 struct PeelShared {
   unsigned int bar_count;
   unsigned int bar_gen;
-  unsigned int fcount[2];   // frontier vertices, by round parity
-  unsigned int ccount[2];   // frontier chunk descriptors, by round parity
+  // per round parity: (frontier vertices << 32) | chunk descriptors, one
+  // 64-bit atomic claims both
+  unsigned long long fc[2];
   unsigned int acount;      // survivors of the current full scan
   int mindeg;               // their minimum degree
 };
@@ -219,16 +242,21 @@ __device__ __forceinline__ void grid_barrier(PeelShared* sh, unsigned int nblock
   __syncthreads();
 }
 
-// frontier vertex v of the round with parity p: ceil(deg/32) descriptors
+// frontier vertex v of the round with parity p: ceil(deg/32) descriptors,
+// each an edge range (start << 6 | length <= 32) -- the decrement needs no
+// further offset loads
 __device__ __forceinline__ void peel_enqueue(const int64_t* __restrict__ ro, int32_t v, int p,
                                              uint64_t* __restrict__ chunks, int64_t cap,
                                              PeelShared* sh) {
-  atomicAdd(&sh->fcount[p], 1u);
-  const unsigned nch = (unsigned)((ro[v + 1] - ro[v] + 31) >> 5);
-  if (nch == 0) return;
-  const unsigned base = atomicAdd(&sh->ccount[p], nch);
-  uint64_t* out = chunks + (size_t)p * cap + base;
-  for (unsigned j = 0; j < nch; ++j) out[j] = ((uint64_t)(uint32_t)v << 32) | j;
+  const int64_t e0 = ro[v], e1 = ro[v + 1];
+  const unsigned nch = (unsigned)((e1 - e0 + 31) >> 5);
+  const unsigned long long old = atomicAdd(&sh->fc[p], (1ull << 32) | nch);
+  uint64_t* out = chunks + (size_t)p * cap + (uint32_t)old;
+  for (unsigned j = 0; j < nch; ++j) {
+    const int64_t st = e0 + 32 * (int64_t)j;
+    const int64_t len = e1 - st < 32 ? e1 - st : 32;
+    out[j] = ((uint64_t)st << 6) | (uint64_t)len;
+  }
 }
 
 __global__ void __launch_bounds__(PEEL_THREADS)
@@ -277,7 +305,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         }
       }
       grid_barrier(sh, G, nothing);
-      nf = *(volatile unsigned int*)&sh->fcount[p];
+      nf = (int64_t)(*(volatile unsigned long long*)&sh->fc[p] >> 32);
       na = *(volatile unsigned int*)&sh->acount;
       const int32_t mn = *(volatile int*)&sh->mindeg;
       int32_t* t = alive;
@@ -292,7 +320,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         continue;
       }
     } else {
-      nf = *(volatile unsigned int*)&sh->fcount[p];
+      nf = (int64_t)(*(volatile unsigned long long*)&sh->fc[p] >> 32);
       if (nf == 0) {  // the level is exhausted
         k += 1;
         full = true;
@@ -305,16 +333,16 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
     if (k > deg_max) deg_max = k;
     // decrement the live neighbours of the frontier; the unique k+1 -> k
     // crossing claims the vertex for round r + 1
-    const int64_t nc = *(volatile unsigned int*)&sh->ccount[p];
+    const int64_t nc = (int64_t)(uint32_t)*(volatile unsigned long long*)&sh->fc[p];
     const uint64_t* cl = chunks + (size_t)p * chunk_cap;
     const uint64_t next_tag = (uint64_t)(r + 1) << 32;
     for (int64_t c = gwarp; c < nc; c += nwarps) {
       const uint64_t dsc = __ldcg(&cl[c]);
-      const int32_t v = (int32_t)(dsc >> 32);
-      const int64_t e = ro[v] + ((int64_t)(uint32_t)dsc << 5) + lane;
-      if (e < ro[v + 1]) {
-        const int32_t u = col[e];
-        if (!__ldcg(&removed[u]) && atomicSub(&deg[u], 1) == k + 1) {
+      if (lane < (int)(dsc & 63)) {
+        const int32_t u = col[(int64_t)(dsc >> 6) + lane];
+        // no removed[] test needed: a peeled vertex has deg <= the level it
+        // left at <= k, so its decrement never returns k + 1
+        if (atomicSub(&deg[u], 1) == k + 1) {
           removed[u] = 1;
           key[u] = next_tag | (uint32_t)u;
           peel_enqueue(ro, u, p ^ 1, chunks, chunk_cap, sh);
@@ -323,8 +351,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
     }
     // every CTA has read this round's counters: they become round r + 2's
     grid_barrier(sh, G, [sh, p] {
-      sh->fcount[p] = 0;
-      sh->ccount[p] = 0;
+      sh->fc[p] = 0;
       sh->acount = 0;
       sh->mindeg = 0x7fffffff;
     });
@@ -561,55 +588,41 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
   uint64_t* keys = nullptr;
   int64_t m = 0;
   if (num_edges > 0) {
-    uint64_t* raw = nullptr;
-    int64_t* d_cnt = nullptr;  // [0] selected count, [1] out-of-range flag
-    if (dev_alloc(&raw, num_edges, s) || dev_alloc(&d_cnt, 2, s)) return -1;
-    MCE_CHECK(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(int64_t), s));
-    k_edge_keys<<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, num_vertices, raw,
-                                                    (int*)(d_cnt + 1));
+    // both directions at once: one sort of 2E keys, then one unique pass
+    // merges duplicates; self-loops are all-ones keys, which sort last
+    const int64_t dk = 2 * num_edges;
+    int64_t* d_cnt = nullptr;  // [0] unique count, [1] out-of-range flag, [2] last key is a loop
+    if (dev_alloc(&keys, dk, s) || dev_alloc(&d_cnt, 3, s)) return -1;
+    MCE_CHECK(cudaMemsetAsync(d_cnt, 0, 3 * sizeof(int64_t), s));
+    k_edge_keys_both<<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, num_vertices,
+                                                         keys, (int*)(d_cnt + 1));
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     dev_free(owned, s);
-    // drop self-loops
-    if (dev_alloc(&keys, num_edges, s)) return -1;
+    if (sort_keys(&keys, dk, 2 * b, s)) return -1;
+    uint64_t* uniq = nullptr;
+    if (dev_alloc(&uniq, dk, s)) return -1;
     size_t tb = 0;
-    MCE_CHECK(cub::DeviceSelect::If(nullptr, tb, raw, keys, d_cnt, num_edges, NotAllOnes(), s));
+    MCE_CHECK(cub::DeviceSelect::Unique(nullptr, tb, keys, uniq, d_cnt, dk, s));
     void* tmp = nullptr;
     MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
-    MCE_CHECK(cub::DeviceSelect::If(tmp, tb, raw, keys, d_cnt, num_edges, NotAllOnes(), s));
+    MCE_CHECK(cub::DeviceSelect::Unique(tmp, tb, keys, uniq, d_cnt, dk, s));
     cudaFreeAsync(tmp, s);
-    int64_t hk[2] = {0, 0};
-    MCE_CHECK(cudaMemcpyAsync(hk, d_cnt, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    k_last_is_loop<<<1, 1, 0, s>>>(uniq, d_cnt, 2 * b);
+    mce_count_launch();
+    int64_t hk[3] = {0, 0, 0};
+    MCE_CHECK(cudaMemcpyAsync(hk, d_cnt, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
-    dev_free(raw, s);
-    const int64_t kept = hk[0];
+    dev_free(keys, s);
+    dev_free(d_cnt, s);
+    keys = uniq;
     if (hk[1]) {
       dev_free(keys, s);
-      dev_free(d_cnt, s);
       delete g;
       mce_set_error("vertex id outside [0, num_vertices)");
       return -2;
     }
-    if (sort_keys(&keys, kept, 2 * b, s)) return -1;
-    // merge duplicates
-    uint64_t* uniq = nullptr;
-    if (dev_alloc(&uniq, kept, s)) return -1;
-    tb = 0;
-    MCE_CHECK(cub::DeviceSelect::Unique(nullptr, tb, keys, uniq, d_cnt, kept, s));
-    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
-    MCE_CHECK(cub::DeviceSelect::Unique(tmp, tb, keys, uniq, d_cnt, kept, s));
-    cudaFreeAsync(tmp, s);
-    MCE_CHECK(cudaMemcpyAsync(&m, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    MCE_CHECK(cudaStreamSynchronize(s));
-    dev_free(keys, s);
-    dev_free(d_cnt, s);
-    // both directions, sorted by (src, dst)
-    if (dev_alloc(&keys, 2 * m, s)) return -1;
-    if (m > 0) k_expand_directed<<<grid_for(m), 256, 0, s>>>(uniq, m, b, keys);
-    mce_count_launch();
-    MCE_CHECK(cudaGetLastError());
-    dev_free(uniq, s);
-    if (sort_keys(&keys, 2 * m, 2 * b, s)) return -1;
+    m = (hk[0] - hk[2]) / 2;  // directed entries come in pairs
   } else {
     dev_free(owned, s);
   }

@@ -300,6 +300,10 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # 2x the 126 MB L2
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    import gc
+
+    gc.collect()
+    gc.disable()  # no collector pauses between the kernels of a timed step
     with ClockSampler(local, enabled=not args.no_clocks) as clocks:
         if world > 1:
             dist.barrier()
@@ -312,6 +316,7 @@ def main():
             kernel_ms += res.kernel_ms
             clocks.sample_now()  # between the events: host time only
         torch.cuda.synchronize()
+    gc.enable()
     launches = _lib.lib().mce_launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     dev_ms = sum(step_ms) / args.steps
@@ -330,6 +335,8 @@ def main():
         if world > 1:
             dist.barrier()
         e2e_ms = 0.0
+        gc.collect()
+        gc.disable()
         for _ in range(args.steps):
             flush.zero_()
             e0.record()
@@ -337,6 +344,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             e2e_ms += e0.elapsed_time(e1)
+        gc.enable()
         e2e_ms /= args.steps
     if world > 1:
         t = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device="cuda")

@@ -101,7 +101,7 @@ typedef struct {
   int measure_bytes;     /* also count the algorithmic CSR bytes of the induced-subgraph
                             builds into mce_run_result.build_bytes (bench only; l1) */
   int partial_xrows_min_w; /* partial mode: build X rows only for bitset classes of at
-                              least this many words (0 -> 4); same traversal either way */
+                              least this many words (0 -> 1); same traversal either way */
 } mce_run_config;
 
 typedef struct {

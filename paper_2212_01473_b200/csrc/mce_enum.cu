@@ -331,14 +331,45 @@ struct Worker {
     }
     if (XROWS) {
       // X rows (induced.py:95-103): X member x is earlier than every P vertex,
-      // so its P-neighbours are N+(x) & P.  Lane t owns column t.
-      for (int t = lane; t < nx; t += 32) {
-        for (int w = 0; w < W; ++w) xrowsT[(size_t)w * a.xcap + t] = 0;
-        const int32_t x = root_x[t];
-        const int64_t lo = a.split[x], hi = a.ro[x + 1];
-        for (int64_t e = lo; e < hi; ++e) {
-          int j = bsearch_i32(plist, np, col[e]);
-          if (j >= 0) xrowsT[(size_t)(j >> 5) * a.xcap + t] |= 1u << (j & 31);
+      // so its P-neighbours are N+(x) & P.  Same flattened (member,
+      // neighbour) walk as the P rows: a root with a huge X (a hub late in
+      // the order) costs sum |N+(x)| / 32 independent loads per lane, not a
+      // serial scan per lane.
+      for (int w = 0; w < W; ++w)
+        for (int t = lane; t < nx; t += 32) xrowsT[(size_t)w * a.xcap + t] = 0;
+      __syncwarp();
+      for (int t0 = 0; t0 < nx; t0 += 32) {
+        const int t = t0 + lane;
+        int64_t lo = 0;
+        int len = 0;
+        if (t < nx) {
+          const int32_t x = root_x[t];
+          lo = a.split[x];
+          len = (int)(a.ro[x + 1] - lo);
+        }
+        int incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int u = __shfl_up_sync(FULLMASK, incl, d);
+          if (lane >= d) incl += u;
+        }
+        const int excl = incl - len;
+        const int total = __shfl_sync(FULLMASK, incl, 31);
+#pragma unroll 2
+        for (int base = 0; base < total; base += 32) {
+          const int k = base + lane;
+          int owner = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
+            if (v <= k) owner += step;
+          }
+          const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
+          const int excl_o = __shfl_sync(FULLMASK, excl, owner);
+          if (k < total) {
+            const int j = bsearch_i32(plist, np, col[lo_o + (k - excl_o)]);
+            if (j >= 0) atomicOr(&xrowsT[(size_t)(j >> 5) * a.xcap + t0 + owner], 1u << (j & 31));
+          }
         }
       }
     }
@@ -380,9 +411,13 @@ struct Worker {
         return false;
       }
     }
-    for (int base = 0; base < live; base += 32) {
-      int i = base + lane;
-      bool hit = (i < live) && xx_adjacent(xx[i], v, gv);
+    for (int base = 0; base < live; base += 128) {  // 4 independent tests per lane in flight
+      bool hit = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32 + lane;
+        hit |= (i < live) && xx_adjacent(xx[i], v, gv);
+      }
       if (__any_sync(FULLMASK, hit)) return true;
     }
     return false;
@@ -390,19 +425,29 @@ struct Worker {
 
   // stable partition of xx[0, live) by adjacency to v (xsets.py:55-82)
   __device__ int partition(int v, int32_t gv, int live) {
+    constexpr int U = 4;  // tokens per lane per iteration: U independent adjacency tests in flight
     int kept = 0, dropped = 0;
     const unsigned lt = (1u << lane) - 1;
-    for (int base = 0; base < live; base += 32) {
-      int i = base + lane;
-      bool valid_i = i < live;
-      int32_t t = valid_i ? xx[i] : 0;
-      bool keep = valid_i && xx_adjacent(t, v, gv);
-      unsigned km = __ballot_sync(FULLMASK, keep);
-      unsigned dm = __ballot_sync(FULLMASK, valid_i && !keep);
-      if (keep) xx[kept + __popc(km & lt)] = t;
-      else if (valid_i) xtmp[dropped + __popc(dm & lt)] = t;
-      kept += __popc(km);
-      dropped += __popc(dm);
+    for (int base = 0; base < live; base += 32 * U) {
+      int32_t t[U];
+      bool ok[U], keep[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * 32 + lane;
+        ok[u] = i < live;
+        t[u] = ok[u] ? xx[i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) keep[u] = ok[u] && xx_adjacent(t[u], v, gv);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // in order: the partition stays stable
+        const unsigned km = __ballot_sync(FULLMASK, keep[u]);
+        const unsigned dm = __ballot_sync(FULLMASK, ok[u] && !keep[u]);
+        if (keep[u]) xx[kept + __popc(km & lt)] = t[u];
+        else if (ok[u]) xtmp[dropped + __popc(dm & lt)] = t[u];
+        kept += __popc(km);
+        dropped += __popc(dm);
+      }
     }
     __syncwarp();
     for (int i = lane; i < dropped; i += 32) xx[kept + i] = xtmp[i];
@@ -570,6 +615,7 @@ struct Worker {
         if (xm && live > 0) {
           if (XROWS) {
             uint32_t adj = 0;  // live X_X members' adjacency, word w
+#pragma unroll 4
             for (int i = lane; i < live; i += 32) adj |= xrowsT[(size_t)w * a.xcap + xx[i]];
             adj = __reduce_or_sync(FULLMASK, adj);
             xm &= ~adj;
@@ -1469,7 +1515,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       const int64_t guess = req > 0 ? req : std::min<int64_t>(metric_slots, cp.count + metric_slots / 4);
       cudaEvent_t* ev = &events[2 * nev++];
       bool xr = false;
-      const int xmin = cfg->partial_xrows_min_w > 0 ? cfg->partial_xrows_min_w : 4;
+      const int xmin = cfg->partial_xrows_min_w > 0 ? cfg->partial_xrows_min_w : 1;
       int rc = launch_mode(cfg->induced_full != 0, cp.W, xmin, args, req, &workers_used, s,
                            &launches, budget, guess, ev, &xr);
       if (rc) {

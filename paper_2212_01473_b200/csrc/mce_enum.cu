@@ -42,6 +42,7 @@ constexpr int HIST_MAX = MCE_HIST_MAX;
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int ROOT_STRIPES = 32;  // root-claim counters (<= 32: one per lane in phase2())
 constexpr int ROOT_STRIDE = 16;   // 128 B apart
+constexpr int XROWS_PARTIAL_MAX = 2048;  // partial mode: X rows for roots with |X| <= this
 
 // Lock-free worker list (paper §3.3, reference scheduler.py:99-165).  A parked
 // worker sets its bit in `idle_bits`; a donor claims a receiver by clearing
@@ -160,6 +161,7 @@ struct Worker {
   const int32_t* root_x;
   int np = 0, nx = 0;
   int64_t origin = 0;
+  bool xr = false;  // X rows built for this root (see build())
   // metrics (uniform across the warp)
   long long nodes = 0, roots_claimed = 0, don_made = 0, don_recv = 0;
   unsigned long long cliques = 0, hash = 0, max_size = 0;
@@ -229,6 +231,7 @@ struct Worker {
   // Fill plist / root_x / rows (and X rows) for root `r`; returns R0 length.
   __device__ int build(int64_t r) {
     const int32_t* col = a.col;
+    xr = false;
     int nr;
     if (a.roots_mode == 1) {
       const int64_t v = r;
@@ -329,7 +332,12 @@ struct Worker {
         }
       }
     }
-    if (XROWS) {
+    // Partial mode builds X rows only when |X| is moderate: a hub late in the
+    // order (|X| in the thousands, tiny P) visits few nodes, and its handful
+    // of X_X scans through the CSR cost less than sum |N+(x)| row-building
+    // loads.  Full mode always needs them (X_X pivot candidates).
+    xr = XROWS && (PIVOT_XX || nx <= XROWS_PARTIAL_MAX);
+    if (xr) {
       // X rows (induced.py:95-103): X member x is earlier than every P vertex,
       // so its P-neighbours are N+(x) & P.  Same flattened (member,
       // neighbour) walk as the P rows: a root with a huge X (a hub late in
@@ -379,7 +387,7 @@ struct Worker {
 
   // ---------------------------------------------------------------- pieces
   __device__ __forceinline__ bool xx_adjacent(int32_t t, int v, int32_t gv) const {
-    if (XROWS) return (xrowsT[(size_t)(v >> 5) * a.xcap + t] >> (v & 31)) & 1u;
+    if (XROWS && xr) return (xrowsT[(size_t)(v >> 5) * a.xcap + t] >> (v & 31)) & 1u;
     const int32_t x = root_x[t];
     return contains_range(a.col, a.split[x], a.ro[x + 1], gv);
   }
@@ -391,7 +399,7 @@ struct Worker {
   // neighbours than there are live members -- look each y in N-(gv) up in
   // the live prefix by binary search.
   __device__ bool xx_any_adjacent(int v, int32_t gv, int live, bool sorted = false) const {
-    if (!XROWS && sorted) {
+    if (!(XROWS && xr) && sorted) {
       const int64_t nb = a.ro[gv], ne = a.split[gv];
       if (ne - nb < live) {
         for (int64_t base = nb; base < ne; base += 32) {
@@ -437,8 +445,50 @@ struct Worker {
         ok[u] = i < live;
         t[u] = ok[u] ? xx[i] : 0;
       }
+      if (XROWS && xr) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) keep[u] = ok[u] && xx_adjacent(t[u], v, gv);
+        for (int u = 0; u < U; ++u) keep[u] = ok[u] && xx_adjacent(t[u], v, gv);
+      } else {
+        // U binary searches of gv in N+(x) in lockstep: U loads in flight per step
+        int64_t lo[U], hi[U];
+        bool hit[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int32_t x = ok[u] ? root_x[t[u]] : 0;
+          lo[u] = ok[u] ? a.split[x] : 0;
+          hi[u] = ok[u] ? a.ro[x + 1] : 0;
+          hit[u] = false;
+        }
+        for (;;) {
+          int32_t val[U];
+          int64_t mid[U];
+          bool act = false;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (lo[u] < hi[u]) {
+              mid[u] = (lo[u] + hi[u]) >> 1;
+              val[u] = a.col[mid[u]];
+              act = true;
+            }
+          }
+          if (!act) break;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (lo[u] < hi[u]) {
+              if (val[u] == gv) {
+                hit[u] = true;
+                lo[u] = hi[u];
+              } else if (val[u] < gv) {
+                lo[u] = mid[u] + 1;
+              } else {
+                hi[u] = mid[u];
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) keep[u] = ok[u] && hit[u];
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {  // in order: the partition stays stable
         const unsigned km = __ballot_sync(FULLMASK, keep[u]);
@@ -613,7 +663,7 @@ struct Worker {
         if (lane == fl) NL.w[k] &= ~lm;
         unsigned xm = __ballot_sync(FULLMASK, xclear);
         if (xm && live > 0) {
-          if (XROWS) {
+          if (XROWS && xr) {
             uint32_t adj = 0;  // live X_X members' adjacency, word w
 #pragma unroll 4
             for (int i = lane; i < live; i += 32) adj |= xrowsT[(size_t)w * a.xcap + xx[i]];

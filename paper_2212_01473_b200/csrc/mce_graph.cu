@@ -10,6 +10,7 @@
 //                                          same degeneracy)
 //   reorder ............ graph.py:213-224
 #include <cub/cub.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -444,6 +445,27 @@ __global__ void k_reorder_keys(const int64_t* __restrict__ ro, const int32_t* __
   }
 }
 
+// ndeg[pos[v]] = deg(v); ndeg[n] = 0 (so an exclusive scan gives n + 1 offsets)
+__global__ void k_permuted_degrees(const int64_t* __restrict__ ro, const int64_t* __restrict__ pos,
+                                   int64_t n, int64_t* __restrict__ ndeg) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    ndeg[v < n ? pos[v] : n] = v < n ? ro[v + 1] - ro[v] : 0;
+}
+
+// one warp per source row: the row's neighbours, relabelled, into row pos[v]
+__global__ void k_scatter_rows(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                               int64_t n, const int64_t* __restrict__ pos,
+                               const int64_t* __restrict__ nro, int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t src = ro[v], len = ro[v + 1] - src, dst = nro[pos[v]];
+    for (int64_t j = lane; j < len; j += 32) out[dst + j] = (int32_t)pos[col[src + j]];
+  }
+}
+
 __global__ void k_relabel(const int64_t* __restrict__ pos, int64_t n,
                           const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -496,7 +518,7 @@ int csr_from_sorted_keys(mce_graph* g, uint64_t* keys, int64_t nnz, int b, cudaS
 
 // Bucket peeling in one persistent launch + one (round, id) sort; positions
 // to d_pos (device).
-int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaStream_t s) {
+int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaStream_t s) {
   const int64_t n = g->n;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
@@ -514,32 +536,46 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* degeneracy, cudaS
   uint8_t* removed = nullptr;
   uint64_t* key = nullptr;
   PeelShared* sh = nullptr;
-  int64_t* d_deg = nullptr;
   // one round's descriptors: sum over its vertices of ceil(deg/32) <= n + 2m/32
   const int64_t chunk_cap = n + g->nnz / 32 + 1;
   if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
       dev_alloc(&chunks, 2 * chunk_cap, s) || dev_alloc(&removed, n, s) ||
-      dev_alloc(&key, n, s) || dev_alloc(&sh, 1, s) || dev_alloc(&d_deg, 1, s))
+      dev_alloc(&key, n, s) || dev_alloc(&sh, 1, s))
     return -1;
   PeelShared init{};
   init.mindeg = 0x7fffffff;
   MCE_CHECK(cudaMemcpyAsync(sh, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   k_peel_persistent<<<(int)grid, PEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2,
                                                       chunks, chunk_cap, removed, key, sh,
-                                                      d_deg);
+                                                      d_degeneracy);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
-  MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   // rounds < n, ids < 2^31: sort the (round, id) keys over the bits they use
   const int rb = bits_for(std::max<int64_t>(n, 2));
   if (sort_keys(&key, n, 32 + rb, s)) return -1;
   k_peel_positions<<<grid_for(n), 256, 0, s>>>(key, n, d_pos);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
-  MCE_CHECK(cudaStreamSynchronize(s));
   dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(chunks, s);
-  dev_free(removed, s); dev_free(key, s); dev_free(sh, s); dev_free(d_deg, s);
+  dev_free(removed, s); dev_free(key, s); dev_free(sh, s);
   return 0;
+}
+
+// Degeneracy order into device buffers (positions, degeneracy); no host sync.
+int order_device(const mce_graph* g, int method, int64_t* d_pos, int64_t* d_deg, cudaStream_t s) {
+  const int64_t n = g->n;
+  if (method == 1) {
+    int64_t leaves = 2;
+    while (leaves < n) leaves <<= 1;
+    uint64_t* tree = nullptr;
+    if (dev_alloc(&tree, 2 * leaves, s)) return -1;
+    k_exact_order<<<1, EXACT_THREADS, 0, s>>>(g->ro, g->col, n, leaves, tree, d_pos, d_deg);
+    mce_count_launch();
+    MCE_CHECK(cudaGetLastError());
+    dev_free(tree, s);
+    return 0;
+  }
+  return peel_parallel(g, d_pos, d_deg, s);
 }
 
 }  // namespace
@@ -733,29 +769,16 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
   *degeneracy = 0;
   if (n == 0) return 0;
   int64_t* d_pos = position_on_device ? position : nullptr;
-  if (!d_pos && dev_alloc(&d_pos, n, s)) return -1;
-  if (method == 1) {
-    int64_t leaves = 2;
-    while (leaves < n) leaves <<= 1;
-    uint64_t* tree = nullptr;
-    int64_t* d_deg = nullptr;
-    if (dev_alloc(&tree, 2 * leaves, s) || dev_alloc(&d_deg, 1, s)) return -1;
-    k_exact_order<<<1, EXACT_THREADS, 0, s>>>(g->ro, g->col, n, leaves, tree, d_pos, d_deg);
-    mce_count_launch();
-    MCE_CHECK(cudaGetLastError());
-    MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    MCE_CHECK(cudaStreamSynchronize(s));
-    dev_free(tree, s);
-    dev_free(d_deg, s);
-  } else {
-    int rc = peel_parallel(g, d_pos, degeneracy, s);
-    if (rc) return rc;
-  }
-  if (!position_on_device) {
+  int64_t* d_deg = nullptr;
+  if ((!d_pos && dev_alloc(&d_pos, n, s)) || dev_alloc(&d_deg, 1, s)) return -1;
+  int rc = order_device(g, method, d_pos, d_deg, s);
+  if (rc) return rc;
+  MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  if (!position_on_device)
     MCE_CHECK(cudaMemcpyAsync(position, d_pos, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
-    MCE_CHECK(cudaStreamSynchronize(s));
-    dev_free(d_pos, s);
-  }
+  MCE_CHECK(cudaStreamSynchronize(s));
+  if (!position_on_device) dev_free(d_pos, s);
+  dev_free(d_deg, s);
   return 0;
 }
 
@@ -776,21 +799,48 @@ int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_dev
     MCE_CHECK(cudaMemcpyAsync(owned, position, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
     d_pos = owned;
   }
-  uint64_t* keys = nullptr;
-  if (dev_alloc(&keys, g->nnz, s)) return -1;
-  if (g->nnz > 0) {
-    k_reorder_keys<<<grid_for(n * 32), 256, 0, s>>>(g->ro, g->col, n, d_pos, b, keys);
+  // Row-wise relabel: the new row pos[v] is v's adjacency mapped through
+  // pos, so the new offsets are a scan of the permuted degrees, the rows are
+  // scattered whole (coalesced), and only each row needs sorting -- a
+  // segmented sort of int32 labels instead of a global sort of 64-bit keys.
+  (void)b;
+  const int64_t nnz = g->nnz;
+  h->nnz = nnz;
+  int64_t* ndeg = nullptr;
+  int32_t* tmpcol = nullptr;
+  if (dev_alloc(&h->ro, n + 1, s) || dev_alloc(&h->col, nnz, s) || dev_alloc(&ndeg, n + 1, s) ||
+      dev_alloc(&tmpcol, nnz, s) || dev_alloc(&h->labels, n, s))
+    return -1;
+  if (n > 0) {
+    k_permuted_degrees<<<grid_for(n + 1), 256, 0, s>>>(g->ro, d_pos, n, ndeg);
+    mce_count_launch();
+    size_t tb = 0;
+    MCE_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ndeg, h->ro, n + 1, s));
+    void* tmp = nullptr;
+    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    MCE_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, ndeg, h->ro, n + 1, s));
+    cudaFreeAsync(tmp, s);
+    if (nnz > 0) {
+      k_scatter_rows<<<grid_for(n * 32), 256, 0, s>>>(g->ro, g->col, n, d_pos, h->ro, tmpcol);
+      mce_count_launch();
+      tb = 0;
+      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmpcol, h->col, nnz, n, h->ro,
+                                                   h->ro + 1, s));
+      MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, tmpcol, h->col, nnz, n, h->ro,
+                                                   h->ro + 1, s));
+      cudaFreeAsync(tmp, s);
+    }
+    k_relabel<<<grid_for(n), 256, 0, s>>>(d_pos, n, g->labels, h->labels);
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
-    if (sort_keys(&keys, g->nnz, 2 * b, s)) return -1;
+  } else {
+    MCE_CHECK(cudaMemsetAsync(h->ro, 0, sizeof(int64_t), s));
   }
-  if (dev_alloc(&h->labels, n, s)) return -1;
-  if (n > 0) k_relabel<<<grid_for(n), 256, 0, s>>>(d_pos, n, g->labels, h->labels);
-  mce_count_launch();
-  MCE_CHECK(cudaGetLastError());
-  int rc = csr_from_sorted_keys(h, keys, g->nnz, b, s);
-  dev_free(keys, s);
+  dev_free(ndeg, s);
+  dev_free(tmpcol, s);
   dev_free(owned, s);
+  int rc = mce_graph_build_split(h, s);
   if (rc) { mce_graph_free(h); return rc; }
   *out = h;
   return 0;
@@ -804,11 +854,15 @@ int mce_preprocess(const mce_graph* g, int method, int64_t* degeneracy, void* st
   cudaStream_t s = (cudaStream_t)stream;
   *out = nullptr;
   *degeneracy = 0;
+  if (g->n == 0) return mce_reorder(g, nullptr, 1, stream, out);
   int64_t* d_pos = nullptr;
-  if (dev_alloc(&d_pos, g->n, s)) return -1;
-  int rc = mce_degeneracy_order(g, method, d_pos, 1, degeneracy, stream);
-  if (!rc) rc = mce_reorder(g, d_pos, 1, stream, out);
+  int64_t* d_deg = nullptr;
+  if (dev_alloc(&d_pos, g->n, s) || dev_alloc(&d_deg, 1, s)) return -1;
+  int rc = order_device(g, method, d_pos, d_deg, s);
+  if (!rc) rc = mce_reorder(g, d_pos, 1, stream, out);  // ends with a stream sync
+  if (!rc) MCE_CHECK(cudaMemcpy(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost));
   dev_free(d_pos, s);
+  dev_free(d_deg, s);
   return rc;
 }
 

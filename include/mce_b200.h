@@ -102,6 +102,9 @@ typedef struct {
                             builds into mce_run_result.build_bytes (bench only; l1) */
   int partial_xrows_min_w; /* partial mode: build X rows only for bitset classes of at
                               least this many words (0 -> 1); same traversal either way */
+  int donation_min_x;    /* B200 extension: also donate a branch whose node has at least
+                            this many live X_X members (0 = off; the reference donates on
+                            |P| >= donation_min_p only).  Scheduling only: same results */
 } mce_run_config;
 
 typedef struct {

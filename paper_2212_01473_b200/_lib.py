@@ -41,6 +41,7 @@ class RunConfigC(ctypes.Structure):
         ("mem_fraction", ctypes.c_double),
         ("measure_bytes", ctypes.c_int),
         ("partial_xrows_min_w", ctypes.c_int),
+        ("donation_min_x", ctypes.c_int),
     ]
 
 

@@ -104,6 +104,7 @@ struct EnumArgs {
   uint32_t* mbits;
   int worker_list_on;
   int min_p;
+  int min_x;  // also donate branches whose node has >= min_x live X_X members (0: off)
 };
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* a, int len, int32_t key) {
@@ -935,7 +936,8 @@ struct Worker {
       for (int k = 0; k < K; ++k) childP.w[k] = P.w[k] & rowv.w[k];
       const int cpop = popc(childP);
       const int32_t gv = plist[v];
-      if (a.worker_list_on && cpop >= a.min_p && below > 0 && any(NL) && phase2()) {
+      if (a.worker_list_on && (cpop >= a.min_p || (a.min_x > 0 && live >= a.min_x)) &&
+          below > 0 && any(NL) && phase2()) {
         B cxp;
 #pragma unroll
         for (int k = 0; k < K; ++k) cxp.w[k] = XP.w[k] & rowv.w[k];
@@ -1560,6 +1562,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.collect_len = collect_len;
       args.worker_list_on = cfg->worker_list;
       args.min_p = cfg->donation_min_p;
+      args.min_x = cfg->donation_min_x;
       int req = cfg->workers > 0 ? cfg->workers : 0;
       if (req <= 0) req = 0;
       const int64_t guess = req > 0 ? req : std::min<int64_t>(metric_slots, cp.count + metric_slots / 4);

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(PEEL_THREADS)
 k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                   int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
                   uint64_t* __restrict__ chunks, int64_t chunk_cap,
-                  uint8_t* __restrict__ removed, uint64_t* __restrict__ key, PeelShared* sh,
+                  uint8_t* __restrict__ removed, uint32_t* __restrict__ key, PeelShared* sh,
                   int64_t* __restrict__ out_degeneracy) {
   const unsigned int G = gridDim.x;
   const int tid = threadIdx.x;
@@ -298,7 +298,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         const int32_t d = __ldcg(&deg[v]);
         if (d <= k) {
           removed[v] = 1;
-          key[v] = ((uint64_t)r << 32) | (uint32_t)v;
+          key[v] = (uint32_t)r;
           peel_enqueue(ro, v, p, chunks, chunk_cap, sh);
         } else {
           alive2[atomicAdd(&sh->acount, 1u)] = v;
@@ -336,7 +336,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
     // crossing claims the vertex for round r + 1
     const int64_t nc = (int64_t)(uint32_t)*(volatile unsigned long long*)&sh->fc[p];
     const uint64_t* cl = chunks + (size_t)p * chunk_cap;
-    const uint64_t next_tag = (uint64_t)(r + 1) << 32;
+    const uint32_t next_round = (uint32_t)(r + 1);
     for (int64_t c = gwarp; c < nc; c += nwarps) {
       const uint64_t dsc = __ldcg(&cl[c]);
       if (lane < (int)(dsc & 63)) {
@@ -345,7 +345,7 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
         // left at <= k, so its decrement never returns k + 1
         if (atomicSub(&deg[u], 1) == k + 1) {
           removed[u] = 1;
-          key[u] = next_tag | (uint32_t)u;
+          key[u] = next_round;
           peel_enqueue(ro, u, p ^ 1, chunks, chunk_cap, sh);
         }
       }
@@ -363,12 +363,19 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
   if (blockIdx.x == 0 && tid == 0) *out_degeneracy = deg_max;
 }
 
-// positions from the sorted (round, id) keys
-__global__ void k_peel_positions(const uint64_t* __restrict__ sorted, int64_t n,
+// ids 0..n-1 (the values of the stable round sort)
+__global__ void k_iota32(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+// position of the i-th vertex of the (round, id) order
+__global__ void k_peel_positions(const int32_t* __restrict__ ids, int64_t n,
                                  int64_t* __restrict__ pos) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    pos[(uint32_t)sorted[i]] = i;
+    pos[ids[i]] = i;
 }
 
 // ---- exact order (reference tie-break): single CTA, min-segment-tree over
@@ -534,7 +541,7 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cud
   int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr;
   uint64_t* chunks = nullptr;
   uint8_t* removed = nullptr;
-  uint64_t* key = nullptr;
+  uint32_t* key = nullptr;  // round of every vertex
   PeelShared* sh = nullptr;
   // one round's descriptors: sum over its vertices of ceil(deg/32) <= n + 2m/32
   const int64_t chunk_cap = n + g->nnz / 32 + 1;
@@ -551,11 +558,28 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cud
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   // rounds < n, ids < 2^31: sort the (round, id) keys over the bits they use
-  const int rb = bits_for(std::max<int64_t>(n, 2));
-  if (sort_keys(&key, n, 32 + rb, s)) return -1;
-  k_peel_positions<<<grid_for(n), 256, 0, s>>>(key, n, d_pos);
-  mce_count_launch();
-  MCE_CHECK(cudaGetLastError());
+  // stable sort of the vertex ids by round (ids enter ascending, so ties stay
+  // in id order); rounds < n bound the key bits
+  {
+    const int rb = bits_for(std::max<int64_t>(n, 2));
+    uint32_t* key2 = nullptr;
+    int32_t *ids = nullptr, *ids2 = nullptr;
+    if (dev_alloc(&key2, n, s) || dev_alloc(&ids, n, s) || dev_alloc(&ids2, n, s)) return -1;
+    k_iota32<<<grid_for(n), 256, 0, s>>>(ids, n);
+    mce_count_launch();
+    cub::DoubleBuffer<uint32_t> dk(key, key2);
+    cub::DoubleBuffer<int32_t> dv(ids, ids2);
+    size_t tb = 0;
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n, 0, rb, s));
+    void* tmp = nullptr;
+    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, n, 0, rb, s));
+    cudaFreeAsync(tmp, s);
+    k_peel_positions<<<grid_for(n), 256, 0, s>>>(dv.Current(), n, d_pos);
+    mce_count_launch();
+    MCE_CHECK(cudaGetLastError());
+    dev_free(key2, s); dev_free(ids, s); dev_free(ids2, s);
+  }
   dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(chunks, s);
   dev_free(removed, s); dev_free(key, s); dev_free(sh, s);
   return 0;

@@ -69,6 +69,10 @@ class RunConfig:
     induced: str = "auto"      # "ip" | "ipx" | "auto"
     worker_list: bool = True
     donation_min_p: int = 10
+    # B200 extension: also donate branches of nodes with this many live X_X
+    # members (a hub root with a tiny P but thousands of excluded vertices is
+    # partition-bound); 0 disables.  Scheduling only -- results are unchanged.
+    donation_min_x: int = 1024
     backoff: Backoff = field(default_factory=Backoff)
     collect_limit: int | None = None
     timing: bool = False
@@ -85,6 +89,8 @@ class RunConfig:
             raise ValueError(f"unknown induced mode {self.induced!r}")
         if self.donation_min_p < 0:
             raise ValueError("donation_min_p must be >= 0")
+        if self.donation_min_x < 0:
+            raise ValueError("donation_min_x must be >= 0")
         if self.backoff.initial <= 0 or self.backoff.max < self.backoff.initial:
             raise ValueError("backoff must satisfy 0 < initial <= max")
 
@@ -189,6 +195,7 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
             mem_fraction=float(os.environ.get("MCE_MEM_FRACTION", "0.5")),
             measure_bytes=int(bool(measure_bytes)),
             partial_xrows_min_w=int(os.environ.get("MCE_PARTIAL_XROWS_MIN_W", "0")),
+            donation_min_x=int(cfg.donation_min_x),
         )
         buf = np.zeros(max(cap_words, 1), dtype=np.int64) if cap_words else None
         wm = np.zeros((slots, 4), dtype=np.int64)

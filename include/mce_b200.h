@@ -10,7 +10,7 @@
  *
  *   reference function                          replaced by
  *   graph.py:103-129   from_edges            ->  mce_graph_from_edges
- *   graph.py:132-180  parse_edge_list (tail)->  mce_graph_from_edges (after host tokenising)
+ *   graph.py:132-180  parse_edge_list       ->  mce_graph_from_text
  *   graph.py:28-64    Graph CSR accessors   ->  mce_graph_from_csr / mce_graph_copy_csr / mce_graph_info
  *   graph.py:183-210  degeneracy_order      ->  mce_degeneracy_order
  *   graph.py:213-224  reorder               ->  mce_reorder
@@ -49,6 +49,18 @@ const char* mce_last_error(void);
  * 2*num_edges int64 values, on the host or (edges_on_device=1) the device. */
 int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
                          int edges_on_device, void* stream, mce_graph** out);
+
+/* Edge-list TEXT -> canonical graph, parsed on the device (graph.py:132-180
+ * parse_edge_list): '#'/'%' comment lines, "%%MatrixMarket" header (1-based
+ * ids after it, the next data line is the size line), two integer tokens per
+ * line, ids compacted to [0, n) ascending.  `text` is `len` bytes on the host
+ * or (text_on_device=1) the device.  On a malformed line returns -2 with
+ * *err_line = its 1-based number and *err_code = 1 (token count),
+ * 2 (non-integer token) or 3 (id below base) -- the reference's
+ * EdgeListParseError cases; *num_vertices = n on success. */
+int mce_graph_from_text(const char* text, int64_t len, int base, int text_on_device,
+                        void* stream, mce_graph** out, int64_t* err_line, int* err_code,
+                        int64_t* num_vertices);
 
 /* Adopt an already canonical CSR (row_offsets: n+1, col_indices: nnz). */
 int mce_graph_from_csr(const int64_t* row_offsets, const int64_t* col_indices, int64_t n,

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmce_b200.so")
-SOURCES = ["mce_graph.cu", "mce_enum.cu", "mce_synth.cu"]
+SOURCES = ["mce_graph.cu", "mce_enum.cu", "mce_synth.cu", "mce_text.cu"]
 HEADERS = ["mce_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

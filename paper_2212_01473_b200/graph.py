@@ -26,7 +26,6 @@ sizes differ.
 from __future__ import annotations
 
 import ctypes
-import io
 from dataclasses import dataclass
 from typing import IO, Iterable
 
@@ -258,45 +257,45 @@ def from_device_edges(edges_dev, num_edges: int, num_vertices: int, stream=None)
     return _from_device(num_vertices, h)
 
 
-def parse_edge_list(source: str | IO[str], base: int = 0, symmetrize: bool = True) -> Graph:
+_PARSE_MESSAGES = {
+    1: "expected two integer tokens, got {!r}",
+    2: "non-integer token in {!r}",
+    3: "vertex id below base in {!r}",
+}
+
+
+def parse_edge_list(source: str | bytes | IO[str] | IO[bytes], base: int = 0,
+                    symmetrize: bool = True) -> Graph:
     """Parse whitespace-separated edge-list text into a canonical graph
-    (reference graph.py:132-180): '#'/'%' comments, MatrixMarket header
+    (reference graph.py:132-180): '#'/'%' comments, a MatrixMarket header
     switches to 1-based ids and skips the size line, ids are compacted to
-    [0, n), duplicates merge, self-loops drop, output always symmetric."""
-    del symmetrize
-    stream = io.StringIO(source) if isinstance(source, str) else source
-    us: list[int] = []
-    vs: list[int] = []
-    matrix_market = False
-    size_pending = False
-    for line_no, line in enumerate(stream, start=1):
-        text = line.strip()
-        if not text:
-            continue
-        if text.startswith("%%MatrixMarket"):
-            matrix_market, size_pending, base = True, True, 1
-            continue
-        if text[0] in "#%":
-            continue
-        if size_pending:
-            size_pending = False
-            continue
-        tok = text.split()
-        if len(tok) < 2 or (len(tok) > 2 and not matrix_market):
-            raise EdgeListParseError(line_no, f"expected two integer tokens, got {text!r}")
-        try:
-            u, v = int(tok[0]) - base, int(tok[1]) - base
-        except ValueError as exc:
-            raise EdgeListParseError(line_no, f"non-integer token in {text!r}") from exc
-        if u < 0 or v < 0:
-            raise EdgeListParseError(line_no, f"vertex id below base in {text!r}")
-        us.append(u)
-        vs.append(v)
-    if not us:
-        return from_edges(np.empty((0, 2), dtype=np.int64), 0)
-    raw = np.column_stack((np.asarray(us, dtype=np.int64), np.asarray(vs, dtype=np.int64)))
-    ids, compact = np.unique(raw, return_inverse=True)
-    return from_edges(compact.reshape(-1, 2).astype(np.int64), len(ids))
+    [0, n), duplicates merge, self-loops drop, output always symmetric.
+
+    The text is parsed on the GPU (``mce_graph_from_text``): lines are found
+    by a device scan, classified and tokenised one thread per line; the
+    first malformed line raises ``EdgeListParseError`` with its number, as
+    in the reference's sequential loop."""
+    del symmetrize  # canonical form is always undirected
+    if base not in (0, 1):
+        raise ValueError("base must be 0 or 1")
+    if isinstance(source, str):
+        data = source.encode()
+    elif isinstance(source, (bytes, bytearray, memoryview)):
+        data = bytes(source)
+    else:
+        raw = source.read()
+        data = raw.encode() if isinstance(raw, str) else bytes(raw)
+    h = ctypes.c_void_p()
+    line = ctypes.c_int64(0)
+    code = ctypes.c_int(0)
+    n = ctypes.c_int64(0)
+    rc = _lib.lib().mce_graph_from_text(data, len(data), int(base), 0, None, ctypes.byref(h),
+                                        ctypes.byref(line), ctypes.byref(code), ctypes.byref(n))
+    if rc == -2 and line.value > 0:
+        text = data.split(b"\n")[line.value - 1].decode(errors="replace").strip()
+        raise EdgeListParseError(line.value, _PARSE_MESSAGES[code.value].format(text))
+    _lib.check(rc, "mce_graph_from_text")
+    return _from_device(int(n.value), h)
 
 
 def degeneracy_order(g: Graph, method: str = "parallel") -> DegeneracyOrder:

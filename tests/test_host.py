@@ -12,7 +12,6 @@ import pytest
 from conftest import golden_cases
 from paper_2212_01473_b200 import generate
 from paper_2212_01473_b200.bk import CliqueSink
-from paper_2212_01473_b200.graph import EdgeListParseError, parse_edge_list
 from paper_2212_01473_b200.metrics import TIME_CATEGORIES, WorkerMetrics, aggregate
 from paper_2212_01473_b200.scheduler import Backoff, RunConfig, choose_induced_mode
 
@@ -73,16 +72,6 @@ def test_metrics_aggregate():
     assert set(rep.category_shares) == set(TIME_CATEGORIES)
     with pytest.raises(ValueError):
         aggregate([])
-
-
-def test_parse_errors_carry_line_numbers():
-    with pytest.raises(EdgeListParseError) as exc:
-        parse_edge_list(io.StringIO("0 1\nnot numbers\n"))
-    assert exc.value.line_no == 2
-    with pytest.raises(EdgeListParseError):
-        parse_edge_list(io.StringIO("0 1 2 3\n"))
-    with pytest.raises(EdgeListParseError):
-        parse_edge_list(io.StringIO("1 2\n0 1\n"), base=1)
 
 
 @pytest.mark.parametrize("case", [c for c in golden_cases() if c["name"].startswith("gnp_")

@@ -112,6 +112,46 @@ def _enumerate_whole_graph(g: Graph, sink: CliqueSink, metrics: dict | None) -> 
     return sink.total
 
 
+ORACLE_MAX_VERTICES = 24
+
+
+def adjacency_masks(g: Graph) -> list[int]:
+    """Neighbourhood of every vertex as an int bit mask (reference bk.py:113-121)."""
+    ro, ci = g.row_offsets, g.col_indices
+    out = []
+    for v in range(g.num_vertices):
+        m = 0
+        for u in ci[ro[v]:ro[v + 1]]:
+            m |= 1 << int(u)
+        out.append(m)
+    return out
+
+
+def oracle_enumerate(g: Graph) -> list[tuple[int, ...]]:
+    """Maximal cliques by testing every vertex subset, for n <= 24 (reference
+    bk.py:212-241): the independent check behind ``mce oracle-check``.  All
+    2^n subsets at once as uint32 masks: a subset is a clique when every
+    member's closed neighbourhood covers it, maximal when no outside vertex
+    is adjacent to all of it."""
+    n = g.num_vertices
+    if n > ORACLE_MAX_VERTICES:
+        raise ValueError(f"oracle limited to {ORACLE_MAX_VERTICES} vertices, got {n}")
+    if n == 0:
+        return []
+    nbr = np.array(adjacency_masks(g), dtype=np.uint32)
+    subsets = np.arange(1 << n, dtype=np.uint32)
+    clique = np.ones(subsets.size, dtype=bool)
+    grow = np.zeros(subsets.size, dtype=bool)
+    for v in range(n):
+        bit = np.uint32(1 << v)
+        member = (subsets & bit) != 0
+        closed = nbr[v] | bit
+        clique &= ~member | ((subsets & ~closed) == 0)
+        grow |= ~member & ((subsets & ~nbr[v]) == 0)
+    keep = subsets[clique & ~grow & (subsets != 0)]
+    return sorted(tuple(v for v in range(n) if (int(s) >> v) & 1) for s in keep)
+
+
 def bk_pivot(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
     """All maximal cliques of ``g`` (reference bk.py:153-183) via the GPU
     engine; cliques are reported in ``g``'s labels."""

@@ -105,6 +105,7 @@ struct EnumArgs {
   int worker_list_on;
   int min_p;
   int min_x;  // also donate branches whose node has >= min_x live X_X members (0: off)
+  int xrows_partial_max;  // partial mode: X rows only for roots with |X| <= this
 };
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* a, int len, int32_t key) {
@@ -337,7 +338,7 @@ struct Worker {
     // order (|X| in the thousands, tiny P) visits few nodes, and its handful
     // of X_X scans through the CSR cost less than sum |N+(x)| row-building
     // loads.  Full mode always needs them (X_X pivot candidates).
-    xr = XROWS && (PIVOT_XX || nx <= XROWS_PARTIAL_MAX);
+    xr = XROWS && (PIVOT_XX || nx <= a.xrows_partial_max);
     if (xr) {
       // X rows (induced.py:95-103): X member x is earlier than every P vertex,
       // so its P-neighbours are N+(x) & P.  Same flattened (member,
@@ -1563,6 +1564,10 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.worker_list_on = cfg->worker_list;
       args.min_p = cfg->donation_min_p;
       args.min_x = cfg->donation_min_x;
+      {
+        const char* e = getenv("MCE_XROWS_PARTIAL_MAX");  // diagnostics override
+        args.xrows_partial_max = e ? atoi(e) : XROWS_PARTIAL_MAX;
+      }
       int req = cfg->workers > 0 ? cfg->workers : 0;
       if (req <= 0) req = 0;
       const int64_t guess = req > 0 ? req : std::min<int64_t>(metric_slots, cp.count + metric_slots / 4);

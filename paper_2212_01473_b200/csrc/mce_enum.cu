@@ -229,6 +229,51 @@ struct Worker {
       r.w[k] = valid(k, lane) ? xrowsT[(size_t)word(k) * a.xcap + t] : 0u;
   }
 
+  // ---------------------------------------------------------------- flat walk
+  // Visit every (member i, entry col[e]) pair of `cnt` members with CSR
+  // ranges range(i) -> (lo, len): 32 members at a time, their ranges
+  // flattened over the lanes (warp scan of the lengths, owner found by a
+  // shuffle binary search), four entries per lane in flight -- so a warp
+  // keeps 128 independent col loads outstanding whatever the degree mix.
+  template <typename RangeF, typename VisitF>
+  __device__ __forceinline__ void flat_walk(int cnt, RangeF range, VisitF visit) const {
+    constexpr int U = 4;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      int64_t lo = 0;
+      int len = 0;
+      if (i0 + lane < cnt) range(i0 + lane, lo, len);
+      int incl = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const int excl = incl - len;
+      const int total = __shfl_sync(FULLMASK, incl, 31);
+      for (int base = 0; base < total; base += 32 * U) {
+        int own[U];
+        int32_t val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = base + u * 32 + lane;
+          int owner = 0;  // lanes q with incl_q <= k
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
+            if (v <= k) owner += step;
+          }
+          own[u] = owner;
+          const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
+          const int excl_o = __shfl_sync(FULLMASK, excl, owner);
+          val[u] = k < total ? a.col[lo_o + (k - excl_o)] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (base + u * 32 + lane < total) visit(i0 + own[u], val[u]);
+      }
+    }
+  }
+
   // ---------------------------------------------------------------- build
   // Fill plist / root_x / rows (and X rows) for root `r`; returns R0 length.
   __device__ int build(int64_t r) {
@@ -291,49 +336,23 @@ struct Worker {
     for (int w = 0; w < W; ++w)
       for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
     __syncwarp();
-    // The (member, neighbour) pairs of 32 members at a time are flattened
-    // over the lanes (warp scan of |N+(a_i)|, owner found by a shuffle
-    // binary search), so every iteration issues 32 independent col loads
-    // whatever the degree mix.
-    for (int i0 = 0; i0 < np; i0 += 32) {
-      const int i = i0 + lane;
-      int64_t lo = 0;
-      int len = 0;
-      if (i < np) {
-        const int32_t ai = plist[i];
-        lo = a.split[ai];
-        len = (int)(a.ro[ai + 1] - lo);
-      }
-      int incl = len;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(FULLMASK, incl, d);
-        if (lane >= d) incl += t;
-      }
-      const int excl = incl - len;
-      const int total = __shfl_sync(FULLMASK, incl, 31);
-      for (int base = 0; base < total; base += 32) {
-        const int k = base + lane;
-        int owner = 0;  // lanes q with incl_q <= k
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
-          if (v <= k) owner += step;
-        }
-        const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
-        const int excl_o = __shfl_sync(FULLMASK, excl, owner);
-        if (k < total) {
-          const int io = i0 + owner;
-          // N+(a_io) & P lies after a_io in the ascending plist
-          const int j = bsearch_i32(plist + io + 1, np - io - 1, col[lo_o + (k - excl_o)]);
+    // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i);
+    // N+(a_i) & P lies after a_i in the ascending plist
+    flat_walk(
+        np,
+        [&](int i, int64_t& lo, int& len) {
+          const int32_t ai = plist[i];
+          lo = a.split[ai];
+          len = (int)(a.ro[ai + 1] - lo);
+        },
+        [&](int io, int32_t w) {
+          const int j = bsearch_i32(plist + io + 1, np - io - 1, w);
           if (j >= 0) {
             const int jj = io + 1 + j;
             atomicOr(&rowsT[(jj >> 5) * CAPP + io], 1u << (jj & 31));
             atomicOr(&rowsT[(io >> 5) * CAPP + jj], 1u << (io & 31));
           }
-        }
-      }
-    }
+        });
     // Partial mode builds X rows only when |X| is moderate: a hub late in the
     // order (|X| in the thousands, tiny P) visits few nodes, and its handful
     // of X_X scans through the CSR cost less than sum |N+(x)| row-building
@@ -348,40 +367,17 @@ struct Worker {
       for (int w = 0; w < W; ++w)
         for (int t = lane; t < nx; t += 32) xrowsT[(size_t)w * a.xcap + t] = 0;
       __syncwarp();
-      for (int t0 = 0; t0 < nx; t0 += 32) {
-        const int t = t0 + lane;
-        int64_t lo = 0;
-        int len = 0;
-        if (t < nx) {
-          const int32_t x = root_x[t];
-          lo = a.split[x];
-          len = (int)(a.ro[x + 1] - lo);
-        }
-        int incl = len;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int u = __shfl_up_sync(FULLMASK, incl, d);
-          if (lane >= d) incl += u;
-        }
-        const int excl = incl - len;
-        const int total = __shfl_sync(FULLMASK, incl, 31);
-#pragma unroll 2
-        for (int base = 0; base < total; base += 32) {
-          const int k = base + lane;
-          int owner = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
-            if (v <= k) owner += step;
-          }
-          const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
-          const int excl_o = __shfl_sync(FULLMASK, excl, owner);
-          if (k < total) {
-            const int j = bsearch_i32(plist, np, col[lo_o + (k - excl_o)]);
-            if (j >= 0) atomicOr(&xrowsT[(size_t)(j >> 5) * a.xcap + t0 + owner], 1u << (j & 31));
-          }
-        }
-      }
+      flat_walk(
+          nx,
+          [&](int t, int64_t& lo, int& len) {
+            const int32_t x = root_x[t];
+            lo = a.split[x];
+            len = (int)(a.ro[x + 1] - lo);
+          },
+          [&](int t, int32_t w) {
+            const int j = bsearch_i32(plist, np, w);
+            if (j >= 0) atomicOr(&xrowsT[(size_t)(j >> 5) * a.xcap + t], 1u << (j & 31));
+          });
     }
     __syncwarp();
     return nr;

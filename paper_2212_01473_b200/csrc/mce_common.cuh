@@ -49,6 +49,43 @@ int mce_graph_build_split(mce_graph* g, cudaStream_t s);
 // reuse HBM instead of returning it to the driver at every synchronisation).
 void mce_prepare_device();
 
+// Scratch arena for the temporaries of one API call: one cached device
+// buffer per device, bump-allocated, so a call makes no cudaMallocAsync /
+// cudaFreeAsync of its own once the arena has grown to the call's demand
+// (host-side driver calls dominate a millisecond-scale job otherwise).  A call
+// that outgrows it takes the overflow from the stream-ordered pool and the
+// arena is re-sized for the next call.  Held by one call at a time; a
+// concurrent call (another thread) falls back to the pool.  The destructor
+// synchronises the stream unless the call already did (mark_synced()).
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t s);
+  ~Scratch();
+  template <typename T>
+  int get(T** p, size_t count) {
+    void* q = nullptr;
+    if (raw(&q, (count ? count : 1) * sizeof(T))) return -1;
+    *p = static_cast<T*>(q);
+    return 0;
+  }
+  int raw(void** p, size_t bytes);
+  size_t reserved() const;  // arena bytes this call may use (already held, not in free memory)
+  void mark_synced() { synced_ = true; }
+
+ private:
+  cudaStream_t s_;
+  int dev_ = 0;
+  bool owner_ = false, synced_ = false;
+  size_t used_ = 0, demand_ = 0;
+  void* extra_[64];
+  int nextra_ = 0;
+};
+
+// Free device memory, cached per device for up to a second: cudaMemGetInfo
+// is a driver round trip that occasionally stalls for milliseconds, too much
+// to pay on every call of a millisecond-scale job.
+size_t mce_free_memory();
+
 // count of this library's own kernel launches (mce_launch_count)
 void mce_count_launch(int64_t k = 1);
 

@@ -28,6 +28,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <mutex>
 #include <cstdlib>
 #include <cstdio>
 #include <vector>
@@ -43,6 +45,16 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int ROOT_STRIPES = 32;  // root-claim counters (<= 32: one per lane in phase2())
 constexpr int ROOT_STRIDE = 16;   // 128 B apart
 constexpr int XROWS_PARTIAL_MAX = 2048;  // partial mode: X rows for roots with |X| <= this
+// First-level roots with |X| >= HEAVY_X_MIN get their X rows from a grid-wide
+// pre-pass (k_heavy_xrows) instead of one warp's walk over sum |N+(x)|: a hub
+// late in the order would otherwise bound the whole launch.  Their pool slot
+// (+1) rides in the root word above ROOT_ID_BITS.
+constexpr int HEAVY_X_MIN = 256;
+constexpr int HEAVY_MAX = 16384;        // heavy slots
+constexpr int HEAVY_UNIT_X = 256;       // X members per pre-pass CTA
+constexpr int HEAVY_UNITS_MAX = 1 << 20;
+constexpr int ROOT_ID_BITS = 40;
+constexpr int64_t ROOT_ID_MASK = (1ll << ROOT_ID_BITS) - 1;
 
 // Lock-free worker list (paper §3.3, reference scheduler.py:99-165).  A parked
 // worker sets its bit in `idle_bits`; a donor claims a receiver by clearing
@@ -106,6 +118,8 @@ struct EnumArgs {
   int min_p;
   int min_x;  // also donate branches whose node has >= min_x live X_X members (0: off)
   int xrows_partial_max;  // partial mode: X rows only for roots with |X| <= this
+  const uint32_t* heavy_rows;  // X rows of the heavy-X roots (k_heavy_xrows), per slot
+  const int64_t* heavy_off;    // word offset of slot h's rows (stride |X| of the root)
 };
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* a, int len, int32_t key) {
@@ -125,6 +139,51 @@ __device__ __forceinline__ bool contains_range(const int32_t* __restrict__ col, 
     if (col[mid] < key) lo = mid + 1; else hi = mid;
   }
   return lo < end && col[lo] == key;
+}
+
+// Visit every (member i, entry col[e]) pair of `cnt` members with CSR
+// ranges range(i) -> (lo, len): 32 members at a time, their ranges
+// flattened over the lanes (warp scan of the lengths, owner found by a
+// shuffle binary search), four entries per lane in flight -- so a warp
+// keeps 128 independent col loads outstanding whatever the degree mix.
+template <typename RangeF, typename VisitF>
+__device__ __forceinline__ void warp_flat_walk(const int32_t* __restrict__ col, int lane, int cnt,
+                                             RangeF range, VisitF visit) {
+  constexpr int U = 4;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    int64_t lo = 0;
+    int len = 0;
+    if (i0 + lane < cnt) range(i0 + lane, lo, len);
+    int incl = len;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(FULLMASK, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int excl = incl - len;
+    const int total = __shfl_sync(FULLMASK, incl, 31);
+    for (int base = 0; base < total; base += 32 * U) {
+      int own[U];
+      int32_t val[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = base + u * 32 + lane;
+        int owner = 0;  // lanes q with incl_q <= k
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
+          if (v <= k) owner += step;
+        }
+        own[u] = owner;
+        const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
+        const int excl_o = __shfl_sync(FULLMASK, excl, owner);
+        val[u] = k < total ? col[lo_o + (k - excl_o)] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * 32 + lane < total) visit(i0 + own[u], val[u]);
+    }
+  }
 }
 
 // Bitsets over the root's P have W 32-bit words; lane l holds words
@@ -153,6 +212,8 @@ struct Worker {
   uint32_t* sBR;
   unsigned int* s_hist;  // 32-bit CTA histogram (native shared atomics), spills at 2^31
   uint32_t* xrowsT;
+  uint32_t* xrows_own;     // this worker's X-row buffer (stride a.xcap)
+  int64_t xstride = 0;     // row-word stride of xrowsT (a.xcap, or |X| for a heavy root's pool rows)
   int32_t* xlist_buf;
   int32_t* xx;
   int32_t* xtmp;
@@ -180,7 +241,9 @@ struct Worker {
       rowsT = a.rows_g + (size_t)wid * W * CAPP;
       plist = a.plist_g + (size_t)wid * CAP;
     }
-    xrowsT = XROWS ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
+    xrows_own = XROWS ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
+    xrowsT = xrows_own;
+    xstride = a.xcap;
     xlist_buf = a.xlist ? a.xlist + (size_t)wid * a.xcap : nullptr;
     xx = a.xx + (size_t)wid * a.xcap;
     xtmp = a.xtmp + (size_t)wid * a.xcap;
@@ -226,60 +289,26 @@ struct Worker {
   __device__ __forceinline__ void xrow_of(int32_t t, B& r) const {
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      r.w[k] = valid(k, lane) ? xrowsT[(size_t)word(k) * a.xcap + t] : 0u;
+      r.w[k] = valid(k, lane) ? xrowsT[(size_t)word(k) * xstride + t] : 0u;
   }
 
   // ---------------------------------------------------------------- flat walk
-  // Visit every (member i, entry col[e]) pair of `cnt` members with CSR
-  // ranges range(i) -> (lo, len): 32 members at a time, their ranges
-  // flattened over the lanes (warp scan of the lengths, owner found by a
-  // shuffle binary search), four entries per lane in flight -- so a warp
-  // keeps 128 independent col loads outstanding whatever the degree mix.
   template <typename RangeF, typename VisitF>
   __device__ __forceinline__ void flat_walk(int cnt, RangeF range, VisitF visit) const {
-    constexpr int U = 4;
-    for (int i0 = 0; i0 < cnt; i0 += 32) {
-      int64_t lo = 0;
-      int len = 0;
-      if (i0 + lane < cnt) range(i0 + lane, lo, len);
-      int incl = len;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(FULLMASK, incl, d);
-        if (lane >= d) incl += t;
-      }
-      const int excl = incl - len;
-      const int total = __shfl_sync(FULLMASK, incl, 31);
-      for (int base = 0; base < total; base += 32 * U) {
-        int own[U];
-        int32_t val[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int k = base + u * 32 + lane;
-          int owner = 0;  // lanes q with incl_q <= k
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int v = __shfl_sync(FULLMASK, incl, owner + step - 1);
-            if (v <= k) owner += step;
-          }
-          own[u] = owner;
-          const int64_t lo_o = __shfl_sync(FULLMASK, lo, owner);
-          const int excl_o = __shfl_sync(FULLMASK, excl, owner);
-          val[u] = k < total ? a.col[lo_o + (k - excl_o)] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (base + u * 32 + lane < total) visit(i0 + own[u], val[u]);
-      }
-    }
+    warp_flat_walk(a.col, lane, cnt, range, visit);
   }
 
   // ---------------------------------------------------------------- build
   // Fill plist / root_x / rows (and X rows) for root `r`; returns R0 length.
-  __device__ int build(int64_t r) {
+  __device__ int build(int64_t r_enc) {
     const int32_t* col = a.col;
     xr = false;
     int nr;
+    // l1 roots carry their heavy-X pool slot (+1) above ROOT_ID_BITS
+    const int64_t r = a.roots_mode == 1 ? (r_enc & ROOT_ID_MASK) : r_enc;
+    const int heavy = a.roots_mode == 1 ? (int)(r_enc >> ROOT_ID_BITS) : 0;
+    xrowsT = xrows_own;
+    xstride = a.xcap;
     if (a.roots_mode == 1) {
       const int64_t v = r;
       const int64_t s = a.split[v];
@@ -329,7 +358,7 @@ struct Worker {
       }
       nr = 2;
     }
-    origin = r;
+    origin = r_enc;
     __syncwarp();
     if (np == 0) return nr;
     // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i)
@@ -357,8 +386,12 @@ struct Worker {
     // order (|X| in the thousands, tiny P) visits few nodes, and its handful
     // of X_X scans through the CSR cost less than sum |N+(x)| row-building
     // loads.  Full mode always needs them (X_X pivot candidates).
-    xr = XROWS && (PIVOT_XX || nx <= a.xrows_partial_max);
-    if (xr) {
+    xr = XROWS && (PIVOT_XX || heavy > 0 || nx <= a.xrows_partial_max);
+    if (xr && heavy > 0) {
+      // a heavy-X root's rows were built by the whole grid (k_heavy_xrows)
+      xrowsT = const_cast<uint32_t*>(a.heavy_rows) + a.heavy_off[heavy - 1];
+      xstride = nx;
+    } else if (xr) {
       // X rows (induced.py:95-103): X member x is earlier than every P vertex,
       // so its P-neighbours are N+(x) & P.  Same flattened (member,
       // neighbour) walk as the P rows: a root with a huge X (a hub late in
@@ -385,7 +418,7 @@ struct Worker {
 
   // ---------------------------------------------------------------- pieces
   __device__ __forceinline__ bool xx_adjacent(int32_t t, int v, int32_t gv) const {
-    if (XROWS && xr) return (xrowsT[(size_t)(v >> 5) * a.xcap + t] >> (v & 31)) & 1u;
+    if (XROWS && xr) return (xrowsT[(size_t)(v >> 5) * xstride + t] >> (v & 31)) & 1u;
     const int32_t x = root_x[t];
     return contains_range(a.col, a.split[x], a.ro[x + 1], gv);
   }
@@ -510,7 +543,7 @@ struct Worker {
     for (int k = 0; k < K; ++k) {
       for (unsigned pm = pmask[k]; pm; pm &= pm - 1) {
         const int j = k * 32 + __ffs(pm) - 1;
-        const uint32_t rw = xrow ? xrowsT[(size_t)j * a.xcap + c] : rowsT[j * CAPP + c];
+        const uint32_t rw = xrow ? xrowsT[(size_t)j * xstride + c] : rowsT[j * CAPP + c];
         cnt += __popc(rw & sP[j]);
       }
     }
@@ -664,7 +697,7 @@ struct Worker {
           if (XROWS && xr) {
             uint32_t adj = 0;  // live X_X members' adjacency, word w
 #pragma unroll 4
-            for (int i = lane; i < live; i += 32) adj |= xrowsT[(size_t)w * a.xcap + xx[i]];
+            for (int i = lane; i < live; i += 32) adj |= xrowsT[(size_t)w * xstride + xx[i]];
             adj = __reduce_or_sync(FULLMASK, adj);
             xm &= ~adj;
           } else {
@@ -983,6 +1016,42 @@ struct Worker {
     }
   }
 
+  // The root's X_X token list.  With X rows, members with no neighbour in P
+  // are left out: every branch adds a P vertex to R, so such an x is dropped
+  // by the first partition anyway, is never adjacent to a branch vertex
+  // (leaf maximality) and never wins the pivot (a zero count is never
+  // strictly better) -- the traversal and the node count are unchanged.
+  // The kept tokens stay ascending.
+  __device__ int init_tokens() {
+    if (!(XROWS && xr)) {
+      for (int t = lane; t < nx; t += 32) xx[t] = t;
+      __syncwarp();
+      return nx;
+    }
+    constexpr int U = 4;
+    const unsigned lt = (1u << lane) - 1;
+    int kept = 0;
+    for (int base = 0; base < nx; base += 32 * U) {
+      bool nz[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = base + u * 32 + lane;
+        uint32_t o = 0;
+        if (t < nx)
+          for (int w = 0; w < W; ++w) o |= xrowsT[(size_t)w * xstride + t];
+        nz[u] = o != 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned m = __ballot_sync(FULLMASK, nz[u]);
+        if (nz[u]) xx[kept + __popc(m & lt)] = base + u * 32 + lane;
+        kept += __popc(m);
+      }
+    }
+    __syncwarp();
+    return kept;
+  }
+
   __device__ void run_root(int64_t r) {
     const int nr = build(r);
     B P, XP;
@@ -997,9 +1066,8 @@ struct Worker {
       P.w[k] = x;
       XP.w[k] = 0u;
     }
-    for (int t = lane; t < nx; t += 32) xx[t] = t;
-    __syncwarp();
-    traverse(P, XP, nx, nr, true);
+    const int nxx = init_tokens();
+    traverse(P, XP, nxx, nr, true);
   }
 
   __device__ void run_donated() {
@@ -1114,12 +1182,64 @@ __device__ __forceinline__ int width_rank(int64_t p) {
   return 7;                // 1
 }
 
+struct HeavyPlan {
+  int enabled;
+  unsigned long long pool_cap;      // words
+  unsigned long long* meta;         // 0 slots taken, 1 pool words reserved, 2 pre-pass CTAs
+  int64_t* vertex;                  // HEAVY_MAX
+  int64_t* off;                     // HEAVY_MAX: word offset of the slot's rows
+  int64_t* unit0;                   // HEAVY_MAX: first pre-pass CTA of the slot
+  int* unit_slot;                   // HEAVY_UNITS_MAX: CTA -> slot
+};
+
+// X rows of the heavy-X first-level roots, HEAVY_UNIT_X members per CTA:
+// rows[(j >> 5) * |X| + t] bit j <=> X member t is adjacent to P member j,
+// i.e. P_j in N+(x_t) (x_t < v < P_j) -- induced.py:95-103, the same rows the
+// per-warp build makes, over the whole grid.  P is staged in shared memory;
+// each warp walks the N+ lists of 32 members flattened over its lanes.
+__global__ void __launch_bounds__(256) k_heavy_xrows(HeavyPlan hp, const int64_t* __restrict__ ro,
+                                                     const int64_t* __restrict__ split,
+                                                     const int32_t* __restrict__ col,
+                                                     uint32_t* __restrict__ pool) {
+  __shared__ int32_t sP[MAX_CAPACITY_BITS];
+  const int slot = hp.unit_slot[blockIdx.x];
+  const int64_t v = hp.vertex[slot];
+  const int64_t ps = split[v], xs = ro[v];
+  const int np = (int)(ro[v + 1] - ps);
+  const int nx = (int)(ps - xs);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) sP[i] = col[ps + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int t0 = (int)((blockIdx.x - hp.unit0[slot]) * HEAVY_UNIT_X) + (threadIdx.x >> 5) * 32;
+  if (t0 >= nx) return;
+  const int cnt = min(32, nx - t0);
+  uint32_t* rows = pool + hp.off[slot];
+  const int32_t pmin = sP[0], pmax = sP[np - 1];
+  warp_flat_walk(
+      col, lane, cnt,
+      [&](int i, int64_t& lo, int& len) {
+        const int32_t x = col[xs + t0 + i];
+        lo = split[x];
+        len = (int)(ro[x + 1] - lo);
+      },
+      [&](int i, int32_t y) {
+        if (y < pmin || y > pmax) return;
+        int lo = 0, hi = np;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sP[mid] < y) lo = mid + 1; else hi = mid;
+        }
+        if (lo < np && sP[lo] == y)
+          atomicOr(&rows[(size_t)(lo >> 5) * nx + t0 + i], 1u << (lo & 31));
+      });
+}
+
 __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
                             const int32_t* __restrict__ col, const int64_t* __restrict__ eoff,
                             int64_t n, int roots_mode, int64_t begin, int64_t stride,
                             int64_t count, uint64_t* __restrict__ keys,
                             int64_t* __restrict__ roots, unsigned long long* __restrict__ classes,
-                            unsigned long long* __restrict__ max_p) {
+                            unsigned long long* __restrict__ max_p, HeavyPlan hp) {
   __shared__ unsigned int s_cls[TRIVIAL_RANK + 1];
   if (threadIdx.x <= TRIVIAL_RANK) s_cls[threadIdx.x] = 0;
   __syncthreads();
@@ -1145,6 +1265,25 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
       roots[i] = (u << 32) | v;
     }
     const int rank = (roots_mode == 1 && p == 0) ? TRIVIAL_RANK : width_rank(p);
+    if (hp.enabled && roots_mode == 1 && p > 0 && x >= HEAVY_X_MIN) {
+      // reserve a slot, pool words (|X| x W) and pre-pass CTAs for this root
+      const unsigned long long slot = atomicAdd(&hp.meta[0], 1ull);
+      if (slot < HEAVY_MAX) {
+        const unsigned long long words = (unsigned long long)x * (1ull << (NUM_WIDTHS - 1 - rank));
+        const unsigned long long off = atomicAdd(&hp.meta[1], words);
+        const unsigned long long units = (x + HEAVY_UNIT_X - 1) / HEAVY_UNIT_X;
+        if (off + words <= hp.pool_cap) {
+          const unsigned long long u0 = atomicAdd(&hp.meta[2], units);
+          if (u0 + units <= HEAVY_UNITS_MAX) {
+            hp.vertex[slot] = r;
+            hp.off[slot] = (int64_t)off;
+            hp.unit0[slot] = (int64_t)u0;
+            for (unsigned long long q = 0; q < units; ++q) hp.unit_slot[u0 + q] = (int)slot;
+            roots[i] = r | ((int64_t)(slot + 1) << ROOT_ID_BITS);
+          }
+        }
+      }
+    }
     uint64_t cost = (uint64_t)(p + 1) * (uint64_t)(p + 1) + (uint64_t)(p + 1) * (uint64_t)x / 8;
     const uint64_t lim = (1ull << 56) - 1;
     if (cost > lim) cost = lim;
@@ -1174,7 +1313,7 @@ __global__ void k_build_bytes(const int64_t* __restrict__ roots, int64_t count,
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < count; i += nwarps) {
-    const int64_t r = roots[i];
+    const int64_t r = roots[i] & ROOT_ID_MASK;
     const int64_t lo = ro[r], sp = split[r], hi = ro[r + 1];
     if (lane == 0) bp += 24 + 4 * (hi - lo);
     for (int64_t e = sp + lane; e < hi; e += 32) {
@@ -1218,7 +1357,7 @@ __global__ void k_trivial_roots(const int64_t* __restrict__ roots, int64_t count
   unsigned long long c = 0, h = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = roots[i];
+    const int64_t v = roots[i] & ROOT_ID_MASK;
     if (ro[v + 1] == ro[v]) {
       c++;
       h += mce_mix64(vhash[v] + MCE_SIZE_SALT);
@@ -1266,6 +1405,23 @@ int dalloc(T** p, size_t count, cudaStream_t s) {
   return 0;
 }
 
+// MCE_TRACE=1: host timestamps of the phases of mce_enumerate on stderr (diagnostics)
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  HostTrace() : on(getenv("MCE_TRACE") != nullptr) { t0 = last = std::chrono::steady_clock::now(); }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[mce_trace] %-22s +%8.3f ms (at %8.3f)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+
+HostTrace* g_tr = nullptr;
+
 struct ClassPlan {
   int W;
   int64_t begin, count;  // slice of the sorted root list
@@ -1273,18 +1429,27 @@ struct ClassPlan {
 
 template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
 int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cudaStream_t s,
-                 int64_t* launches, size_t mem_budget, cudaEvent_t* ev, bool* xrows_used) {
+                 int64_t* launches, size_t mem_budget, cudaEvent_t* ev, bool* xrows_used,
+                 Scratch& scr) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
   auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
   constexpr int SPW = W < 32 ? 32 : W;
   size_t smem = HIST_SMEM * sizeof(unsigned int) + 3 * WARPS * SPW * sizeof(uint32_t) +
                 (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
-  MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0, per_sm = 0;
+  if (g_tr) g_tr->mark("class start");
+  int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem));
+  static int per_sm_cache[64];  // per instantiation and device: attribute + occupancy once
+  static bool have[64];
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!have[dev]) {
+    MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cache[dev], kern, WARPS * 32, smem));
+    have[dev] = true;
+  }
+  const int per_sm = per_sm_cache[dev];
   if (per_sm < 1) {
     mce_set_error("enumerate kernel W=%d does not fit on an SM", W);
     return -3;
@@ -1302,6 +1467,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
                       (XROWS ? sizeof(uint32_t) * (size_t)W * xcap : 0) +
                       (args.roots_mode == 2 ? sizeof(int32_t) * xcap : 0) +
                       (ROWS_SMEM ? 0 : sizeof(uint32_t) * (size_t)(W * CAPP + CAP));
+  if (g_tr) g_tr->mark("class occupancy");
   int64_t by_mem = std::max<int64_t>(1, (int64_t)(mem_budget / per_worker));
   int64_t workers = requested_workers > 0 ? requested_workers : resident;
   workers = std::min<int64_t>(workers, resident);
@@ -1312,12 +1478,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   args.levels = (int)levels;
   args.xcap = xcap;
   *workers_used = std::max<int64_t>(*workers_used, workers);
-  std::vector<void*> owned;
-  auto get = [&](auto** p, size_t count) -> int {
-    if (dalloc(p, count, s)) return -1;
-    owned.push_back((void*)*p);
-    return 0;
-  };
+  auto get = [&](auto** p, size_t count) -> int { return scr.get(p, count); };
   if (get(&args.stack, (size_t)workers * levels * 4 * W) || get(&args.lpx, (size_t)workers * levels) ||
       get(&args.rpath, (size_t)workers * (levels + 2)) || get(&args.hsum, (size_t)workers * (levels + 2)) ||
       get(&args.xx, (size_t)workers * xcap) || get(&args.xtmp, (size_t)workers * xcap) ||
@@ -1335,6 +1496,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   if (!ROWS_SMEM && (get(&args.rows_g, (size_t)workers * W * CAPP) ||
                      get(&args.plist_g, (size_t)workers * CAP)))
     return -1;
+  if (g_tr) g_tr->mark("class buffers");
   MCE_CHECK(cudaMemsetAsync(args.wl, 0, sizeof(WorkerListDev), s));
   MCE_CHECK(cudaMemsetAsync(args.wl_wake, 0, sizeof(int) * workers, s));
   MCE_CHECK(cudaMemsetAsync(args.idle_bits, 0, sizeof(unsigned) * ((workers + 31) / 32), s));
@@ -1342,6 +1504,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   MCE_CHECK(cudaMemsetAsync(args.root_counter, 0,
                             sizeof(unsigned long long) * ROOT_STRIPES * ROOT_STRIDE, s));
   const int grid = (int)((workers + WARPS - 1) / WARPS);
+  if (g_tr) g_tr->mark("class memsets");
   MCE_CHECK(cudaEventRecord(ev[0], s));
   kern<<<grid, WARPS * 32, smem, s>>>(args);
   mce_count_launch();
@@ -1349,22 +1512,21 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   *xrows_used = XROWS;
   MCE_CHECK(cudaGetLastError());
   (*launches)++;
-  for (void* p : owned) cudaFreeAsync(p, s);
   return 0;
 }
 
 template <bool PIVOT_XX, bool XROWS>
 int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, int64_t* launches,
-             size_t budget, cudaEvent_t* ev, bool* xr) {
+             size_t budget, cudaEvent_t* ev, bool* xr, Scratch& scr) {
   switch (W) {
-    case 1: return launch_class<1, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr);
-    case 2: return launch_class<2, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr);
-    case 4: return launch_class<4, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr);
-    case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget, ev, xr);
-    case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget, ev, xr);
-    case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
-    case 64: return launch_class<64, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
-    case 128: return launch_class<128, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr);
+    case 1: return launch_class<1, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 2: return launch_class<2, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 4: return launch_class<4, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 64: return launch_class<64, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 128: return launch_class<128, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
   }
   mce_set_error("unsupported bitset width %d", W);
   return -3;
@@ -1376,15 +1538,15 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
 // dependent loads.  Full mode ("ipx") always has them.
 int launch_mode(bool full, int W, int xrows_min_w, EnumArgs args, int workers, int64_t* used,
                 cudaStream_t s, int64_t* launches, size_t budget, int64_t resident_guess,
-                cudaEvent_t* ev, bool* xr) {
-  if (full) return launch_W<true, true>(W, args, workers, used, s, launches, budget, ev, xr);
+                cudaEvent_t* ev, bool* xr, Scratch& scr) {
+  if (full) return launch_W<true, true>(W, args, workers, used, s, launches, budget, ev, xr, scr);
   const size_t xrows_bytes = sizeof(uint32_t) * (size_t)W * (size_t)std::max<int64_t>(args.xcap, 1) *
                              (size_t)std::max<int64_t>(resident_guess, 1);
   // small-|P| roots visit few nodes: building X rows (|X| x |N+(x)| loads)
   // costs more than the CSR look-ups it saves
   if (W >= xrows_min_w && xrows_bytes <= budget / 2)
-    return launch_W<false, true>(W, args, workers, used, s, launches, budget, ev, xr);
-  return launch_W<false, false>(W, args, workers, used, s, launches, budget, ev, xr);
+    return launch_W<false, true>(W, args, workers, used, s, launches, budget, ev, xr, scr);
+  return launch_W<false, false>(W, args, workers, used, s, launches, budget, ev, xr, scr);
 }
 
 }  // namespace
@@ -1394,6 +1556,9 @@ extern "C" {
 int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collect,
                   int64_t* worker_metrics, int64_t worker_metrics_cap, mce_run_result* out,
                   void* stream) {
+  HostTrace tr;
+  g_tr = &tr;
+  struct TrReset { ~TrReset() { g_tr = nullptr; } } tr_reset;
   mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   memset(out, 0, sizeof(*out));
@@ -1403,16 +1568,11 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   }
   const int64_t n = g->n;
   if (n == 0) return 0;
-  std::vector<void*> owned;
-  auto get = [&](auto** p, size_t count) -> int {
-    if (dalloc(p, count, s)) return -1;
-    owned.push_back((void*)*p);
-    return 0;
-  };
-  auto cleanup = [&]() {
-    for (void* p : owned) cudaFreeAsync(p, s);
-    owned.clear();
-  };
+  tr.mark("enter");
+  Scratch scr(s);  // every temporary of this call (released after the final sync)
+  tr.mark("scratch");
+  auto get = [&](auto** p, size_t count) -> int { return scr.get(p, count); };
+  auto cleanup = [&]() {};
   // --- root list ---------------------------------------------------------
   int64_t* eoff = nullptr;
   int64_t total_roots = n;
@@ -1425,9 +1585,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     size_t tb = 0;
     MCE_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, later, eoff + 1, n, s));
     void* tmp = nullptr;
-    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    if (scr.raw(&tmp, tb)) return -1;
     MCE_CHECK(cub::DeviceScan::InclusiveSum(tmp, tb, later, eoff + 1, n, s));
-    cudaFreeAsync(tmp, s);
     MCE_CHECK(cudaMemcpyAsync(&total_roots, eoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MCE_CHECK(cudaStreamSynchronize(s));
   }
@@ -1461,25 +1620,54 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   unsigned long long* bb = nullptr;
   if (get(&bb, 1)) return -1;
   MCE_CHECK(cudaMemsetAsync(bb, 0, sizeof(unsigned long long), s));
-  cudaEvent_t events[2 * NUM_WIDTHS];
+  // timing events, created once per device (one call at a time uses them: the
+  // call holds them until its final synchronisation)
+  static cudaEvent_t ev_cache[64][2 * NUM_WIDTHS];
+  static bool ev_have[64];
+  static std::mutex ev_mu;
+  std::unique_lock<std::mutex> ev_lock(ev_mu);
+  int ev_dev = 0;
+  cudaGetDevice(&ev_dev);
+  if (ev_dev < 0 || ev_dev >= 64) ev_dev = 0;
+  if (!ev_have[ev_dev]) {
+    for (int e = 0; e < 2 * NUM_WIDTHS; ++e) MCE_CHECK(cudaEventCreate(&ev_cache[ev_dev][e]));
+    ev_have[ev_dev] = true;
+  }
+  cudaEvent_t* events = ev_cache[ev_dev];
   int nev = 0;
-  for (int e = 0; e < 2 * NUM_WIDTHS; ++e) cudaEventCreate(&events[e]);
-  struct EvGuard {
-    cudaEvent_t* e;
-    ~EvGuard() { for (int i = 0; i < 2 * NUM_WIDTHS; ++i) cudaEventDestroy(e[i]); }
-  } ev_guard{events};
+  tr.mark("vhash+events");
   if (count > 0) {
     uint64_t *keys = nullptr, *keys2 = nullptr;
     int64_t *roots = nullptr, *roots2 = nullptr;
     unsigned long long* cls = nullptr;
+    constexpr int HMETA = MAXP_SLOT + 1;  // cls[HMETA .. HMETA+2] = heavy plan counters
     if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count) ||
-        get(&cls, MAXP_SLOT + 1)) {
+        get(&cls, HMETA + 3)) {
       cleanup();
       return -1;
     }
-    MCE_CHECK(cudaMemsetAsync(cls, 0, (MAXP_SLOT + 1) * sizeof(unsigned long long), s));
+    MCE_CHECK(cudaMemsetAsync(cls, 0, (HMETA + 3) * sizeof(unsigned long long), s));
+    HeavyPlan hp{};
+    // device memory this call may use: free HBM plus the scratch arena it holds
+    size_t avail_b = 0;
+    avail_b = mce_free_memory() + scr.reserved();
+    tr.mark("memgetinfo");
+    {
+      const size_t free_b = avail_b;
+      const char* e = getenv("MCE_HEAVY");  // diagnostics: MCE_HEAVY=0 disables the pre-pass
+      hp.enabled = cfg->roots == 1 && !(e && atoi(e) == 0) && g->max_earlier >= HEAVY_X_MIN;
+      hp.pool_cap = std::min<unsigned long long>(free_b / 16, 1ull << 30) / sizeof(uint32_t);
+      hp.meta = cls + HMETA;
+      if (hp.enabled && (get(&hp.vertex, HEAVY_MAX) || get(&hp.off, HEAVY_MAX) ||
+                         get(&hp.unit0, HEAVY_MAX) || get(&hp.unit_slot, HEAVY_UNITS_MAX))) {
+        cleanup();
+        return -1;
+      }
+    }
+    tr.mark("setup");
     k_root_keys<<<grid_for(count), 256, 0, s>>>(g->ro, g->split, g->col, eoff, n, cfg->roots,
-                                                 begin, stride, count, keys, roots, cls, cls + MAXP_SLOT);
+                                                 begin, stride, count, keys, roots, cls, cls + MAXP_SLOT,
+                                                 hp);
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(keys, keys2);
@@ -1487,13 +1675,28 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     size_t tb = 0;
     MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, count, 0, 64, s));
     void* tmp = nullptr;
-    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    if (scr.raw(&tmp, tb)) return -1;
     MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 64, s));
-    cudaFreeAsync(tmp, s);
-    unsigned long long hc[MAXP_SLOT + 1];
+    unsigned long long hc[HMETA + 3];
     MCE_CHECK(cudaMemcpyAsync(hc, cls, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    tr.mark("root keys+sort queued");
     MCE_CHECK(cudaStreamSynchronize(s));
+    tr.mark("class counts synced");
     const int64_t* sorted_roots = dv.Current();
+    // heavy-X roots: their X rows over the whole grid, before the enumeration
+    uint32_t* heavy_pool = nullptr;
+    const unsigned long long heavy_units = std::min<unsigned long long>(hc[HMETA + 2], HEAVY_UNITS_MAX);
+    if (hp.enabled && heavy_units > 0) {
+      const unsigned long long words = std::min<unsigned long long>(hc[HMETA + 1], hp.pool_cap);
+      if (get(&heavy_pool, words)) {
+        cleanup();
+        return -1;
+      }
+      MCE_CHECK(cudaMemsetAsync(heavy_pool, 0, words * sizeof(uint32_t), s));
+      k_heavy_xrows<<<(unsigned)heavy_units, 256, 0, s>>>(hp, g->ro, g->split, g->col, heavy_pool);
+      mce_count_launch();
+      MCE_CHECK(cudaGetLastError());
+    }
     // diagnostics: MCE_PROFILE_ROOTS=<file> dumps (root, W, cycles) per root
     const char* prof_path = getenv("MCE_PROFILE_ROOTS");
     long long* prof_cycles = nullptr;
@@ -1521,10 +1724,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     const int64_t trivial_begin = i;  // first-level roots with P empty
     const int64_t trivial_count = count - i;
     int64_t wcap = 0;
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
     double frac = cfg->mem_fraction > 0 ? cfg->mem_fraction : 0.5;
-    size_t budget = (size_t)(free_b * frac);
+    size_t budget = (size_t)(avail_b * frac);
     // per-worker metrics accumulate across class launches
     int64_t metric_slots = 0;
     {
@@ -1560,6 +1761,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.worker_list_on = cfg->worker_list;
       args.min_p = cfg->donation_min_p;
       args.min_x = cfg->donation_min_x;
+      args.heavy_rows = heavy_pool;
+      args.heavy_off = hp.off;
       {
         const char* e = getenv("MCE_XROWS_PARTIAL_MAX");  // diagnostics override
         args.xrows_partial_max = e ? atoi(e) : XROWS_PARTIAL_MAX;
@@ -1571,7 +1774,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       bool xr = false;
       const int xmin = cfg->partial_xrows_min_w > 0 ? cfg->partial_xrows_min_w : 1;
       int rc = launch_mode(cfg->induced_full != 0, cp.W, xmin, args, req, &workers_used, s,
-                           &launches, budget, guess, ev, &xr);
+                           &launches, budget, guess, ev, &xr, scr);
+      tr.mark("class launched");
       if (rc) {
         cleanup();
         return rc;
@@ -1595,7 +1799,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       if (FILE* f = fopen(prof_path, "wb")) {
         for (const ClassPlan& cp : plan)
           for (int64_t i = cp.begin; i < cp.begin + cp.count; ++i) {
-            const int64_t rec[3] = {rts[i], (int64_t)cp.W, (int64_t)cyc[i]};
+            const int64_t rec[3] = {rts[i] & ROOT_ID_MASK, (int64_t)cp.W, (int64_t)cyc[i]};
             fwrite(rec, sizeof(rec), 1, f);
           }
         fclose(f);
@@ -1630,7 +1834,9 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   MCE_CHECK(cudaMemcpyAsync(h_acc, acc, sizeof(h_acc), cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaMemcpyAsync(out->hist, hist, sizeof(int64_t) * HIST_MAX, cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaMemcpyAsync(&h_len, collect_len, sizeof(h_len), cudaMemcpyDeviceToHost, s));
+  tr.mark("results queued");
   MCE_CHECK(cudaStreamSynchronize(s));
+  tr.mark("results synced");
   if (collect && cfg->collect_cap > 0) {
     int64_t words = std::min<int64_t>((int64_t)h_len, cfg->collect_cap);
     if (words > 0)
@@ -1644,6 +1850,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
                                 cudaMemcpyDeviceToHost, s));
   }
   MCE_CHECK(cudaStreamSynchronize(s));
+  scr.mark_synced();
   out->cliques = (int64_t)h_acc[0];
   out->hash = (uint64_t)h_acc[1];
   out->nodes = (int64_t)h_acc[2] + trivial_nodes;
@@ -1662,6 +1869,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   }
   out->kernel_ms = kernel_ms;
   cleanup();
+  tr.mark("done");
   return 0;
 }
 

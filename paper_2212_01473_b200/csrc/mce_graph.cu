@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <vector>
@@ -46,6 +48,91 @@ void mce_prepare_device() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done[dev] = true;
+}
+
+namespace {
+struct ArenaState {
+  std::mutex mu;
+  bool busy = false;
+  char* base = nullptr;
+  size_t cap = 0, want = 0;
+};
+ArenaState g_arena[64];
+constexpr size_t ARENA_ALIGN = 256;
+}  // namespace
+
+namespace {
+bool g_free_stale[64];  // set when the scratch arena re-sizes itself
+}
+
+size_t mce_free_memory() {
+  static std::mutex mu;
+  static size_t cached[64];
+  static std::chrono::steady_clock::time_point at[64];
+  static bool have[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto now = std::chrono::steady_clock::now();
+  if (!have[dev] || g_free_stale[dev] || now - at[dev] > std::chrono::seconds(1)) {
+    g_free_stale[dev] = false;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    cached[dev] = free_b;
+    at[dev] = now;
+    have[dev] = true;
+  }
+  return cached[dev];
+}
+
+Scratch::Scratch(cudaStream_t s) : s_(s) {
+  if (cudaGetDevice(&dev_) != cudaSuccess || dev_ < 0 || dev_ >= 64) return;
+  ArenaState& a = g_arena[dev_];
+  std::lock_guard<std::mutex> lk(a.mu);
+  if (a.busy) return;
+  a.busy = true;
+  owner_ = true;
+  if (a.want > a.cap) {  // grow (the previous call left the arena idle: it synchronised)
+    if (a.base) cudaFree(a.base);
+    a.base = nullptr;
+    a.cap = 0;
+    if (cudaMalloc((void**)&a.base, a.want) == cudaSuccess) a.cap = a.want;
+    else a.base = nullptr;
+    g_free_stale[dev_] = true;
+  }
+}
+
+size_t Scratch::reserved() const { return owner_ ? g_arena[dev_].cap : 0; }
+
+int Scratch::raw(void** p, size_t bytes) {
+  bytes = (bytes + ARENA_ALIGN - 1) / ARENA_ALIGN * ARENA_ALIGN;
+  demand_ += bytes;
+  if (owner_) {
+    ArenaState& a = g_arena[dev_];
+    if (a.base && used_ + bytes <= a.cap) {
+      *p = a.base + used_;
+      used_ += bytes;
+      return 0;
+    }
+  }
+  if (nextra_ >= 64) {
+    mce_set_error("scratch: too many overflow allocations");
+    return -1;
+  }
+  MCE_CHECK(cudaMallocAsync(p, bytes, s_));
+  extra_[nextra_++] = *p;
+  return 0;
+}
+
+Scratch::~Scratch() {
+  if (!synced_) cudaStreamSynchronize(s_);
+  for (int i = 0; i < nextra_; ++i) cudaFreeAsync(extra_[i], s_);
+  if (owner_) {
+    ArenaState& a = g_arena[dev_];
+    std::lock_guard<std::mutex> lk(a.mu);
+    if (demand_ > a.cap) a.want = demand_ + demand_ / 8;
+    a.busy = false;
+  }
 }
 
 namespace {

@@ -136,3 +136,28 @@ def test_parallel_peel_positions_match_restatement(name):
     # preprocess (device-resident positions) agrees with the host-visible order
     _, order, st = preprocess(g)
     assert np.array_equal(order.position, pos) and st.degeneracy == d
+
+
+@pytest.mark.parametrize("induced", ["ip", "ipx"])
+def test_heavy_x_prepass_matches_per_warp_build_and_oracle(induced, monkeypatch):
+    """Hubs late in the order (|X| >= 256) take their X rows from the grid-wide
+    pre-pass (k_heavy_xrows) and start with the zero-row X members left out;
+    the traversal must be the per-warp build's exactly (MCE_HEAVY=0), node
+    count included, and the oracle's."""
+    edges, n = generate.workload_edges("ba200k")
+    g2, _, st = preprocess(from_edges(edges, n))
+    assert g2.device_info()["max_earlier"] >= 4096
+    fast = run(g2, st, RunConfig(induced=induced, worker_list=False))
+    monkeypatch.setenv("MCE_HEAVY", "0")
+    slow = run(g2, st, RunConfig(induced=induced, worker_list=False))
+    monkeypatch.delenv("MCE_HEAVY")
+    assert (fast.clique_count, fast.nodes_total, fast.clique_hash, fast.size_histogram) == \
+        (slow.clique_count, slow.nodes_total, slow.clique_hash, slow.size_histogram)
+    orc = oracle.enumerate_cliques(g2.row_offsets, g2.col_indices, roots="l1", induced=induced,
+                                   degeneracy=st.degeneracy, labels=g2.labels)
+    assert (fast.clique_count, fast.nodes_total, fast.clique_hash_hex) == \
+        (orc["count"], orc["nodes"], orc["hash"])
+    # with donations (hub branches handed to idle warps) the clique set is unchanged
+    don = run(g2, st, RunConfig(induced=induced, donation_min_p=1, donation_min_x=16))
+    assert (don.clique_count, don.clique_hash, don.nodes_total) == \
+        (fast.clique_count, fast.clique_hash, fast.nodes_total)

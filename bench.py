@@ -381,7 +381,7 @@ def main():
                    "max_degree": st.max_degree, "roots": cfg.roots,
                    "induced": res.induced_mode, "root_stride": stride,
                    "maximal_cliques": count, "nodes": nodes, "clique_hash": chash,
-                   "ordering": "parallel peel", "sharding": args.shard if world > 1 else None,
+                   "ordering": "async peel (degeneracy order, no rounds inside a level)", "sharding": args.shard if world > 1 else None,
                    "l2_flush": "256 MiB buffer zeroed between timed steps, outside the "
                                "CUDA events"},
         "e2e": ({"value": count / (e2e_ms / 1e3), "unit": "cliques/s", "ms_per_step": e2e_ms,

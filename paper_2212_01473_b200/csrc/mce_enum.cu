@@ -1237,7 +1237,7 @@ __global__ void __launch_bounds__(256) k_heavy_xrows(HeavyPlan hp, const int64_t
 __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
                             const int32_t* __restrict__ col, const int64_t* __restrict__ eoff,
                             int64_t n, int roots_mode, int64_t begin, int64_t stride,
-                            int64_t count, uint64_t* __restrict__ keys,
+                            int64_t count, uint32_t* __restrict__ keys,
                             int64_t* __restrict__ roots, unsigned long long* __restrict__ classes,
                             unsigned long long* __restrict__ max_p, HeavyPlan hp) {
   __shared__ unsigned int s_cls[TRIVIAL_RANK + 1];
@@ -1284,10 +1284,12 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
         }
       }
     }
-    uint64_t cost = (uint64_t)(p + 1) * (uint64_t)(p + 1) + (uint64_t)(p + 1) * (uint64_t)x / 8;
-    const uint64_t lim = (1ull << 56) - 1;
-    if (cost > lim) cost = lim;
-    keys[i] = ((uint64_t)rank << 56) | (lim - cost);
+    // 24-bit key: class in the top 4 bits, then the cost estimate descending
+    // as the top 20 bits of its float encoding (monotonic for positive
+    // floats: 8 exponent + 12 mantissa bits) -- a 3-pass radix sort
+    const float cost = (float)(p + 1) * (float)(p + 1) + (float)(p + 1) * (float)x * 0.125f;
+    const uint32_t cb = __float_as_uint(cost) >> 11;
+    keys[i] = ((uint32_t)rank << 20) | (0xFFFFFu - (cb & 0xFFFFFu));
     // warp-aggregated: one shared atomic per distinct class in the warp
     const unsigned peers = __match_any_sync(__activemask(), rank);
     if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_cls[rank], (unsigned)__popc(peers));
@@ -1637,7 +1639,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int nev = 0;
   tr.mark("vhash+events");
   if (count > 0) {
-    uint64_t *keys = nullptr, *keys2 = nullptr;
+    uint32_t *keys = nullptr, *keys2 = nullptr;
     int64_t *roots = nullptr, *roots2 = nullptr;
     unsigned long long* cls = nullptr;
     constexpr int HMETA = MAXP_SLOT + 1;  // cls[HMETA .. HMETA+2] = heavy plan counters
@@ -1670,13 +1672,13 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
                                                  hp);
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
-    cub::DoubleBuffer<uint64_t> dk(keys, keys2);
+    cub::DoubleBuffer<uint32_t> dk(keys, keys2);
     cub::DoubleBuffer<int64_t> dv(roots, roots2);
     size_t tb = 0;
-    MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, count, 0, 64, s));
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, count, 0, 24, s));
     void* tmp = nullptr;
     if (scr.raw(&tmp, tb)) return -1;
-    MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 64, s));
+    MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 24, s));
     unsigned long long hc[HMETA + 3];
     MCE_CHECK(cudaMemcpyAsync(hc, cls, sizeof(hc), cudaMemcpyDeviceToHost, s));
     tr.mark("root keys+sort queued");

@@ -450,6 +450,252 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
   if (blockIdx.x == 0 && tid == 0) *out_degeneracy = deg_max;
 }
 
+// ---- asynchronous peel (method 2): no rounds inside a level.  A level k
+// starts with a scan of the alive list that claims every live vertex with
+// degree <= k; from then on the claimed vertices' adjacency is consumed as a
+// task queue of 32-edge chunks by every warp of the grid, and a decrement
+// that takes a neighbour from k+1 to k claims it on the spot (its chunks are
+// appended to the queue).  The level ends at quiescence -- every claimed
+// chunk processed -- detected on ONE packed word (chunks claimed << 32 |
+// chunks done).  Positions are handed out at claim time, so a vertex's later
+// neighbours are exactly those that had not decremented it yet: at most k,
+// a valid degeneracy order (graph.py:183-210's invariant) with the same
+// degeneracy, in a data-dependent order (tie-breaks differ from run to run).
+// Per level: two grid barriers instead of one per peel round.
+constexpr int APEEL_THREADS = 256;
+#ifndef MCE_APEEL_BATCH
+#define MCE_APEEL_BATCH 8
+#endif
+constexpr int APEEL_BATCH = MCE_APEEL_BATCH;  // queue slots a warp reserves at once
+constexpr unsigned long long TASK_EMPTY = ~0ull;
+
+struct APeelShared {
+  alignas(128) unsigned int bar_count;
+  unsigned int bar_gen;
+  alignas(128) unsigned long long tclaim;  // chunks claimed (producers need the old value)
+  alignas(128) unsigned long long tdone;   // chunks processed (no-return adds)
+  alignas(128) unsigned long long head;    // queue slots reserved by consumers
+  alignas(128) unsigned int vclaim;        // positions handed out
+  alignas(128) unsigned int acount;        // scan survivors
+  int mindeg;
+  unsigned int scan_claims;
+};
+
+template <typename F>
+__device__ __forceinline__ void agrid_barrier(APeelShared* sh, unsigned int nblocks, F reset) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = &sh->bar_gen;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(&sh->bar_count, 1u) == nblocks - 1) {
+      reset();
+      sh->bar_count = 0;
+      __threadfence();
+      atomicAdd(&sh->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Claim the lanes' vertices (cnt[lane] of them in cand[0..cnt)): positions
+// from vclaim, chunk descriptors appended to the queue; `done` processed
+// chunks are retired in the same atomic as the new chunks are claimed (same
+// word: the claims are counted before the work that found them is retired).
+template <int MAXC>
+__device__ __forceinline__ void apeel_claim(const int64_t* __restrict__ ro, const int32_t (&cand)[MAXC],
+                                            int cnt, unsigned done, APeelShared* sh,
+                                            uint64_t* __restrict__ tasks, int32_t* __restrict__ order,
+                                            uint8_t* __restrict__ removed, int lane) {
+  int nch = 0;
+  int64_t e0[MAXC];
+#pragma unroll
+  for (int t = 0; t < MAXC; ++t) {
+    if (t < cnt) {
+      const int32_t v = cand[t];
+      e0[t] = ro[v];
+      nch += (int)((ro[v + 1] - e0[t] + 31) >> 5);
+    }
+  }
+  int ic = cnt, in = nch;  // inclusive warp scans of vertices and chunks
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, ic, d);
+    const int b = __shfl_up_sync(0xffffffffu, in, d);
+    if (lane >= d) {
+      ic += a;
+      in += b;
+    }
+  }
+  const int tv = __shfl_sync(0xffffffffu, ic, 31);
+  const int tc = __shfl_sync(0xffffffffu, in, 31);
+  if (tv == 0 && done == 0) return;
+  unsigned vpos = 0;
+  unsigned long long old = 0;
+  if (lane == 0 && tv) {
+    vpos = atomicAdd(&sh->vclaim, (unsigned)tv);
+    old = atomicAdd(&sh->tclaim, (unsigned long long)tc);
+  }
+  // the processed chunks are retired only after the chunks they produced are
+  // counted (tclaim's returned value is consumed first), so done <= claimed
+  // holds at every instant
+  if (tv == 0) {
+    if (lane == 0 && done) atomicAdd(&sh->tdone, (unsigned long long)done);
+    return;
+  }
+  vpos = __shfl_sync(0xffffffffu, vpos, 0);
+  const unsigned long long tpos = __shfl_sync(0xffffffffu, old, 0);
+  unsigned vp = vpos + (unsigned)(ic - cnt);
+  unsigned long long tp = tpos + (unsigned)(in - nch);
+#pragma unroll
+  for (int t = 0; t < MAXC; ++t) {
+    if (t < cnt) {
+      const int32_t v = cand[t];
+      order[vp++] = v;
+      removed[v] = 1;
+      const int64_t e1 = ro[v + 1];
+      for (int64_t st = e0[t]; st < e1; st += 32) {
+        const int64_t len = e1 - st < 32 ? e1 - st : 32;
+        tasks[tp++] = ((uint64_t)st << 6) | (uint64_t)len;
+      }
+    }
+  }
+  if (lane == 0 && done) atomicAdd(&sh->tdone, (unsigned long long)done);
+}
+
+__global__ void __launch_bounds__(APEEL_THREADS)
+k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+             int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
+             uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
+             int32_t* __restrict__ order, APeelShared* sh, int64_t* __restrict__ out_degeneracy,
+             unsigned poll_mask, unsigned sleep_ns) {
+  const unsigned int G = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * APEEL_THREADS + threadIdx.x;
+  const int64_t gstride = (int64_t)G * APEEL_THREADS;
+  auto nothing = [] {};
+  for (int64_t v = gtid; v < n; v += gstride) {
+    deg[v] = (int32_t)(ro[v + 1] - ro[v]);
+    alive_a[v] = (int32_t)v;
+    removed[v] = 0;
+  }
+  agrid_barrier(sh, G, nothing);
+  int32_t* alive = alive_a;
+  int32_t* alive2 = alive_b;
+  int64_t na = n;
+  int32_t k = 0, deg_max = 0;
+  for (;;) {
+    // ---- scan: claim every live vertex with deg <= k (degrees are stable here)
+    for (int64_t base = gtid - lane; base < na; base += gstride) {
+      const int64_t i = base + lane;
+      int32_t v = -1, d = 0x7fffffff;
+      bool take = false, keep = false;
+      if (i < na) {
+        v = __ldcg(&alive[i]);
+        if (!__ldcg(&removed[v])) {
+          d = __ldcg(&deg[v]);
+          take = d <= k;
+          keep = !take;
+        }
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (km) {
+        unsigned o = 0;
+        if (lane == 0) o = atomicAdd(&sh->acount, (unsigned)__popc(km));
+        o = __shfl_sync(0xffffffffu, o, 0);
+        if (keep) alive2[o + __popc(km & ((1u << lane) - 1))] = v;
+        const int md = __reduce_min_sync(0xffffffffu, keep ? d : 0x7fffffff);
+        if (lane == 0) atomicMin(&sh->mindeg, md);
+      }
+      const unsigned tm = __ballot_sync(0xffffffffu, take);
+      if (tm) {
+        if (lane == 0) atomicAdd(&sh->scan_claims, (unsigned)__popc(tm));
+        int32_t c1[1] = {v};
+        apeel_claim<1>(ro, c1, take ? 1 : 0, 0u, sh, tasks, order, removed, lane);
+      }
+    }
+    agrid_barrier(sh, G, nothing);
+    const unsigned claims = *(volatile unsigned*)&sh->scan_claims;
+    const unsigned vc = *(volatile unsigned*)&sh->vclaim;
+    const int32_t mn = *(volatile int*)&sh->mindeg;
+    na = *(volatile unsigned*)&sh->acount;
+    {
+      int32_t* t = alive;
+      alive = alive2;
+      alive2 = t;
+    }
+    if (claims) deg_max = max(deg_max, k);
+    if ((int64_t)vc >= n) break;  // every position handed out
+    if (claims == 0) {
+      k = max(k + 1, mn);
+      agrid_barrier(sh, G, [sh] {
+        sh->acount = 0;
+        sh->mindeg = 0x7fffffff;
+      });
+      continue;
+    }
+    // ---- asynchronous phase: consume chunks until quiescence
+    const int32_t kp1 = k + 1;
+    bool over = false;
+    while (!over) {
+      unsigned long long h = 0;
+      if (lane == 0) h = atomicAdd(&sh->head, (unsigned long long)APEEL_BATCH);
+      h = __shfl_sync(0xffffffffu, h, 0);
+      int got = 0;
+      while (got < APEEL_BATCH) {
+        uint64_t dsc = TASK_EMPTY;
+        int c = 0;
+        for (unsigned polls = 0;; ++polls) {
+          dsc = lane < APEEL_BATCH - got ? __ldcv(&tasks[h + got + lane]) : TASK_EMPTY;
+          const unsigned av = __ballot_sync(0xffffffffu, dsc != TASK_EMPTY);
+          c = __ffs(~av) - 1;  // available prefix of the reservation
+          if (c > 0) break;
+          if ((polls & poll_mask) == poll_mask) {
+            // done first, then claimed: equal values mean nothing was in
+            // flight at the second read (done <= claimed, both monotonic)
+            const unsigned long long dn = __ldcv(&sh->tdone);
+            const unsigned long long cl = __ldcv(&sh->tclaim);
+            if ((cl == dn && h + got >= cl) || __ldcv(&sh->vclaim) >= (unsigned)n) {
+              over = true;
+              break;
+            }
+          }
+          if (sleep_ns) __nanosleep(sleep_ns);
+        }
+        if (over) break;
+        // c chunks: lane l takes edge l of each; c decrements in flight per lane
+        int32_t cand[APEEL_BATCH];
+        int cnt = 0;
+        int32_t u[APEEL_BATCH];
+#pragma unroll
+        for (int t = 0; t < APEEL_BATCH; ++t) {
+          const uint64_t dt = __shfl_sync(0xffffffffu, dsc, t);
+          u[t] = -1;
+          if (t < c && lane < (int)(dt & 63)) u[t] = col[(int64_t)(dt >> 6) + lane];
+        }
+#pragma unroll
+        for (int t = 0; t < APEEL_BATCH; ++t) {
+          if (u[t] >= 0 && atomicSub(&deg[u[t]], 1) == kp1) cand[cnt++] = u[t];
+        }
+        apeel_claim<APEEL_BATCH>(ro, cand, cnt, (unsigned)c, sh, tasks, order, removed, lane);
+        got += c;
+      }
+    }
+    // the next scan runs on quiescent degrees; consumers restart at the queue end
+    agrid_barrier(sh, G, [sh] {
+      sh->head = sh->tclaim;
+      sh->scan_claims = 0;
+      sh->acount = 0;
+      sh->mindeg = 0x7fffffff;
+    });
+    k += 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
+}
+
 // ids 0..n-1 (the values of the stable round sort)
 __global__ void k_iota32(int32_t* __restrict__ out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -672,6 +918,57 @@ int peel_parallel(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cud
   return 0;
 }
 
+unsigned apeel_env(const char* name, unsigned dflt) {  // diagnostics knobs
+  const char* e = getenv(name);
+  return e ? (unsigned)atoi(e) : dflt;
+}
+
+// Asynchronous peel (method 2); positions to d_pos straight from the claim order.
+int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaStream_t s) {
+  const int64_t n = g->n;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int per_sm = -1;
+  if (per_sm < 0)
+    MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_async, APEEL_THREADS, 0));
+  if (per_sm < 1) {
+    mce_set_error("async peel kernel does not fit on an SM");
+    return -3;
+  }
+  const char* e = getenv("MCE_APEEL_CTAS_PER_SM");  // diagnostics
+  const int want = e ? atoi(e) : 2;
+  int64_t grid = std::min<int64_t>((int64_t)std::min(per_sm, std::max(want, 1)) * sms,
+                                   std::max<int64_t>(1, (n + 127) / 128));
+  int32_t *deg = nullptr, *alive = nullptr, *alive2 = nullptr, *order = nullptr;
+  uint64_t* tasks = nullptr;
+  uint8_t* removed = nullptr;
+  APeelShared* sh = nullptr;
+  const int64_t task_cap = n + g->nnz / 32 + 2 * APEEL_BATCH * grid * (APEEL_THREADS / 32) + 64;
+  if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
+      dev_alloc(&order, n, s) || dev_alloc(&tasks, task_cap, s) || dev_alloc(&removed, n, s) ||
+      dev_alloc(&sh, 1, s))
+    return -1;
+  MCE_CHECK(cudaMemsetAsync(tasks, 0xff, sizeof(uint64_t) * task_cap, s));
+  MCE_CHECK(cudaMemsetAsync(sh, 0, sizeof(APeelShared), s));
+  {
+    const int big = 0x7fffffff;
+    MCE_CHECK(cudaMemcpyAsync(&sh->mindeg, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
+  k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
+                                                   removed, order, sh, d_degeneracy,
+                                                   apeel_env("MCE_APEEL_POLL", 7),
+                                                   apeel_env("MCE_APEEL_SLEEP", 64));
+  mce_count_launch();
+  MCE_CHECK(cudaGetLastError());
+  k_peel_positions<<<grid_for(n), 256, 0, s>>>(order, n, d_pos);
+  mce_count_launch();
+  MCE_CHECK(cudaGetLastError());
+  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(order, s);
+  dev_free(tasks, s); dev_free(removed, s); dev_free(sh, s);
+  return 0;
+}
+
 // Degeneracy order into device buffers (positions, degeneracy); no host sync.
 int order_device(const mce_graph* g, int method, int64_t* d_pos, int64_t* d_deg, cudaStream_t s) {
   const int64_t n = g->n;
@@ -686,6 +983,7 @@ int order_device(const mce_graph* g, int method, int64_t* d_pos, int64_t* d_deg,
     dev_free(tree, s);
     return 0;
   }
+  if (method == 2) return peel_async(g, d_pos, d_deg, s);
   return peel_parallel(g, d_pos, d_deg, s);
 }
 

@@ -9,11 +9,17 @@ the reference's dataclass are materialised only when host code reads them.
 
 ``degeneracy_order`` takes ``method``:
 
-* ``"parallel"`` (default) -- bucket peeling on the GPU: every vertex whose
+* ``"parallel"`` -- bucket peeling on the GPU: every vertex whose
   current degree is at most the peel level leaves in the same round, ranked
   by id.  A valid degeneracy ordering with exactly the reference's
   degeneracy ``d`` (so |P| <= d for every first-level root), but not the same
   permutation.
+* ``"async"`` -- peeling without rounds inside a level: the claimed
+  vertices' adjacency is a device-wide task queue, and a vertex is claimed
+  (and given its position) the moment a decrement takes its degree to the
+  level.  A valid degeneracy ordering with the reference's degeneracy, in a
+  data-dependent order that can differ from run to run; the fastest method
+  and the default.
 * ``"exact"`` -- the reference's own order (minimum current degree, ties to
   the smallest id; graph.py:183-210), computed by a single-CTA kernel;
   positions are bit-identical to the reference.
@@ -33,7 +39,7 @@ import numpy as np
 
 from paper_2212_01473_b200 import _lib
 
-ORDER_METHODS = {"parallel": 0, "exact": 1}
+ORDER_METHODS = {"parallel": 0, "exact": 1, "async": 2}
 
 
 class EdgeListParseError(ValueError):
@@ -298,7 +304,7 @@ def parse_edge_list(source: str | bytes | IO[str] | IO[bytes], base: int = 0,
     return _from_device(int(n.value), h)
 
 
-def degeneracy_order(g: Graph, method: str = "parallel") -> DegeneracyOrder:
+def degeneracy_order(g: Graph, method: str = "async") -> DegeneracyOrder:
     """Degeneracy ordering on the GPU (reference graph.py:183-210); see the
     module docstring for ``method``."""
     if method not in ORDER_METHODS:
@@ -342,7 +348,7 @@ def stats(g: Graph, order: DegeneracyOrder) -> GraphStats:
                       degeneracy=order.degeneracy)
 
 
-def preprocess(g: Graph, method: str = "parallel") -> tuple[Graph, DegeneracyOrder, GraphStats]:
+def preprocess(g: Graph, method: str = "async") -> tuple[Graph, DegeneracyOrder, GraphStats]:
     """Order, relabel and summarise in one step (reference graph.py:239-243).
 
     One device call (``mce_preprocess``): the permutation never leaves HBM;

@@ -134,7 +134,7 @@ def test_parallel_peel_positions_match_restatement(name):
     assert got.degeneracy == d
     assert np.array_equal(got.position, pos)
     # preprocess (device-resident positions) agrees with the host-visible order
-    _, order, st = preprocess(g)
+    _, order, st = preprocess(g, method="parallel")
     assert np.array_equal(order.position, pos) and st.degeneracy == d
 
 
@@ -161,3 +161,59 @@ def test_heavy_x_prepass_matches_per_warp_build_and_oracle(induced, monkeypatch)
     don = run(g2, st, RunConfig(induced=induced, donation_min_p=1, donation_min_x=16))
     assert (don.clique_count, don.clique_hash, don.nodes_total) == \
         (fast.clique_count, fast.clique_hash, fast.nodes_total)
+
+
+def _later_counts(ro, ci, pos):
+    src = np.repeat(np.arange(len(ro) - 1), np.diff(ro))
+    later = pos[ci] > pos[src]
+    return np.bincount(src[later], minlength=len(ro) - 1)
+
+
+@pytest.mark.parametrize("name", ["er2k", "ba200k", "planted1m"])
+def test_async_peel_is_a_degeneracy_order(name):
+    """method="async" (no rounds inside a level): a permutation whose every
+    vertex has at most d later neighbours, d the reference's degeneracy --
+    checked on repeated runs, since its tie-breaks are data-dependent -- and
+    the same clique set as the other orders."""
+    from paper_2212_01473_b200 import degeneracy_order
+
+    edges, n = generate.workload_edges(name)
+    g = from_edges(edges, n)
+    ro, ci = g.row_offsets, g.col_indices
+    _, d = oracle.degeneracy_order(ro, ci)
+    for _ in range(3):
+        got = degeneracy_order(g, method="async")
+        assert got.degeneracy == d
+        assert np.array_equal(np.sort(got.position), np.arange(n))
+        assert _later_counts(ro, ci, got.position).max() == d
+    g_a, _, st_a = preprocess(g, method="async")
+    g_p, _, st_p = preprocess(g, method="parallel")
+    assert st_a.degeneracy == st_p.degeneracy == d
+    ra, rp = run(g_a, st_a, RunConfig()), run(g_p, st_p, RunConfig())
+    assert (ra.clique_count, ra.clique_hash, ra.size_histogram) == \
+        (rp.clique_count, rp.clique_hash, rp.size_histogram)
+
+
+def test_async_peel_on_reference_graphs():
+    """Every golden graph of the reference's tests: valid degeneracy order,
+    exact degeneracy, and the reference's clique count / hash."""
+    from conftest import golden_cases
+    from paper_2212_01473_b200 import degeneracy_order
+
+    for case in golden_cases():
+        n = case["n"]
+        edges = np.asarray(case["edges"], dtype=np.int64).reshape(-1, 2)
+        g = from_edges(edges, n)
+        if n == 0:
+            continue
+        got = degeneracy_order(g, method="async")
+        _, d = oracle.degeneracy_order(g.row_offsets, g.col_indices)
+        assert got.degeneracy == d, case["name"]
+        assert np.array_equal(np.sort(got.position), np.arange(n)), case["name"]
+        if g.num_edges:
+            assert _later_counts(g.row_offsets, g.col_indices, got.position).max() == d, case["name"]
+        g2, _, st = preprocess(g, method="async")
+        res = run(g2, st, RunConfig())
+        exp = case["runs"]["l1-ipx"]
+        assert res.clique_count == exp["count"], case["name"]
+        assert res.clique_hash_hex == exp["hash"], case["name"]

@@ -73,6 +73,9 @@ struct Mailbox {
   int32_t rlen;     // R path length, written into the receiver's rpath
   int32_t nxx;      // live X_X tokens, written into the receiver's xx
   int32_t has_task;
+  int32_t owner;    // worker whose buffers hold the root's induced rows
+  int32_t np, nx;   // the root's |P| and |X|
+  int32_t xr;       // X rows in use for the root
   int32_t pad;
 };  // the branch's P and X_P bitsets go to EnumArgs::mbits (2W words per worker)
 
@@ -114,6 +117,8 @@ struct EnumArgs {
   int* wl_wake;
   Mailbox* mbox;
   uint32_t* mbits;
+  uint32_t* pub;  // shared-memory-row classes: per worker, the root's rows + plist published
+                  // for the receivers of its branches (W * CAPP + CAP words)
   int worker_list_on;
   int min_p;
   int min_x;  // also donate branches whose node has >= min_x live X_X members (0: off)
@@ -225,6 +230,13 @@ struct Worker {
   int np = 0, nx = 0;
   int64_t origin = 0;
   bool xr = false;  // X rows built for this root (see build())
+  // Donated branches borrow the root's induced rows instead of rebuilding
+  // them: every donation happens in phase 2 (all roots claimed), after which
+  // no worker builds into its buffers again, so the root owner's rows (its
+  // global rows, or for shared-memory classes the copy it publishes before
+  // its first donation) and X rows stay valid until the launch ends.
+  int owner_wid = 0;
+  bool published = false;
   // metrics (uniform across the warp)
   long long nodes = 0, roots_claimed = 0, don_made = 0, don_recv = 0;
   unsigned long long cliques = 0, hash = 0, max_size = 0;
@@ -359,6 +371,12 @@ struct Worker {
       nr = 2;
     }
     origin = r_enc;
+    owner_wid = wid;
+    published = false;
+    if (!ROWS_SMEM) {
+      rowsT = a.rows_g + (size_t)wid * W * CAPP;
+      plist = a.plist_g + (size_t)wid * CAP;
+    }
     __syncwarp();
     if (np == 0) return nr;
     // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i)
@@ -831,11 +849,22 @@ struct Worker {
         mbits[W + word(q)] = childXP.w[q];
       }
     }
+    if (ROWS_SMEM && !published) {  // first donation from this root: publish its rows
+      uint32_t* pb = a.pub + (size_t)wid * (W * CAPP + CAP);
+      for (int w = 0; w < W; ++w)
+        for (int c = lane; c < np; c += 32) pb[w * CAPP + c] = rowsT[w * CAPP + c];
+      for (int c = lane; c < np; c += 32) pb[W * CAPP + c] = plist[c];
+      published = true;
+    }
     if (lane == 0) {
       rr[rlen] = gv;
       mb->origin = origin;
       mb->rlen = rlen + 1;
       mb->nxx = k;
+      mb->owner = owner_wid;
+      mb->np = np;
+      mb->nx = nx;
+      mb->xr = xr ? 1 : 0;
       mb->has_task = 1;
     }
     __threadfence();
@@ -1070,6 +1099,41 @@ struct Worker {
     traverse(P, XP, nxx, nr, true);
   }
 
+  // Take over the root of a donated branch from its owner's buffers (no
+  // CSR walks): rows and plist (shared-memory classes copy the owner's
+  // published copy into their own shared memory), X rows in place.
+  __device__ void adopt(const Mailbox* mb, int64_t r_enc) {
+    const int owner = mb->owner;
+    np = mb->np;
+    nx = mb->nx;
+    xr = mb->xr != 0;
+    origin = r_enc;
+    owner_wid = owner;
+    published = true;
+    const int64_t r = a.roots_mode == 1 ? (r_enc & ROOT_ID_MASK) : r_enc;
+    const int heavy = a.roots_mode == 1 ? (int)(r_enc >> ROOT_ID_BITS) : 0;
+    root_x = a.roots_mode == 1 ? a.col + a.ro[r] : a.xlist + (size_t)owner * a.xcap;
+    if (ROWS_SMEM) {
+      const uint32_t* pb = a.pub + (size_t)owner * (W * CAPP + CAP);
+      for (int w = 0; w < W; ++w)
+        for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = pb[w * CAPP + c];
+      for (int c = lane; c < np; c += 32) plist[c] = (int32_t)pb[W * CAPP + c];
+    } else {
+      rowsT = a.rows_g + (size_t)owner * W * CAPP;
+      plist = a.plist_g + (size_t)owner * CAP;
+    }
+    if (XROWS && xr) {
+      if (heavy > 0) {
+        xrowsT = const_cast<uint32_t*>(a.heavy_rows) + a.heavy_off[heavy - 1];
+        xstride = nx;
+      } else {
+        xrowsT = a.xrows + (size_t)owner * W * a.xcap;
+        xstride = a.xcap;
+      }
+    }
+    __syncwarp();
+  }
+
   __device__ void run_donated() {
     const Mailbox* mb = a.mbox + wid;
     const uint32_t* mbits = a.mbits + (size_t)wid * 2 * W;
@@ -1082,19 +1146,7 @@ struct Worker {
       P.w[k] = valid(k, lane) ? mbits[word(k)] : 0u;
       XP.w[k] = valid(k, lane) ? mbits[W + word(k)] : 0u;
     }
-    // rebuild the origin's induced rows; rpath/xx were written by the donor,
-    // so save the donated path across build()'s R0 write
-    int32_t keep0 = 0, keep1 = 0;
-    if (lane == 0) {
-      keep0 = rpath[0];
-      keep1 = rpath[1];
-    }
-    build(r);
-    if (lane == 0) {
-      rpath[0] = keep0;
-      rpath[1] = keep1;
-    }
-    __syncwarp();
+    adopt(mb, r);
     traverse(P, XP, nxx, rlen, false);
   }
 };
@@ -1468,7 +1520,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
                       sizeof(long long) * 4 +
                       (XROWS ? sizeof(uint32_t) * (size_t)W * xcap : 0) +
                       (args.roots_mode == 2 ? sizeof(int32_t) * xcap : 0) +
-                      (ROWS_SMEM ? 0 : sizeof(uint32_t) * (size_t)(W * CAPP + CAP));
+                      sizeof(uint32_t) * (size_t)(W * CAPP + CAP);  // rows_g+plist_g, or pub
   if (g_tr) g_tr->mark("class occupancy");
   int64_t by_mem = std::max<int64_t>(1, (int64_t)(mem_budget / per_worker));
   int64_t workers = requested_workers > 0 ? requested_workers : resident;
@@ -1495,6 +1547,9 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   args.plist_g = nullptr;
   if (XROWS && get(&args.xrows, (size_t)workers * W * xcap)) return -1;
   if (args.roots_mode == 2 && get(&args.xlist, (size_t)workers * xcap)) return -1;
+  args.pub = nullptr;
+  if (ROWS_SMEM && args.worker_list_on && get(&args.pub, (size_t)workers * (W * CAPP + CAP)))
+    return -1;
   if (!ROWS_SMEM && (get(&args.rows_g, (size_t)workers * W * CAPP) ||
                      get(&args.plist_g, (size_t)workers * CAP)))
     return -1;

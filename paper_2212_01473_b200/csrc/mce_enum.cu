@@ -556,13 +556,26 @@ struct Worker {
 
   // number of P members adjacent to candidate column c (lane-private c)
   __device__ __forceinline__ int count_in_p(const unsigned (&pmask)[K], int c, bool xrow) const {
+    // row words of up to RB P-words in flight at once (wide classes keep
+    // their rows in global memory: one dependent load per word otherwise)
+    constexpr int RB = W >= 8 ? 4 : 1;
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      for (unsigned pm = pmask[k]; pm; pm &= pm - 1) {
-        const int j = k * 32 + __ffs(pm) - 1;
-        const uint32_t rw = xrow ? xrowsT[(size_t)j * xstride + c] : rowsT[j * CAPP + c];
-        cnt += __popc(rw & sP[j]);
+      for (unsigned pm = pmask[k]; pm;) {
+        int j[RB];
+        uint32_t rw[RB];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+          j[u] = pm ? k * 32 + __ffs(pm) - 1 : -1;
+          pm &= pm - 1;
+        }
+#pragma unroll
+        for (int u = 0; u < RB; ++u)
+          rw[u] = j[u] < 0 ? 0u : (xrow ? xrowsT[(size_t)j[u] * xstride + c] : rowsT[j[u] * CAPP + c]);
+#pragma unroll
+        for (int u = 0; u < RB; ++u)
+          if (j[u] >= 0) cnt += __popc(rw[u] & sP[j[u]]);
       }
     }
     return cnt;
@@ -692,14 +705,27 @@ struct Worker {
         if (cand) {
           uint32_t pin = 0, xin = 0;
 #pragma unroll
+          constexpr int RB = W >= 8 ? 4 : 1;  // row words in flight (see count_in_p)
           for (int q = 0; q < K; ++q) {
-            for (unsigned um = umask[q]; um; um &= um - 1) {
-              const int j = q * 32 + __ffs(um) - 1;
-              const uint32_t below = j < w ? 0xffffffffu : (j == w ? (1u << lane) - 1u : 0u);
-              const uint32_t r = rowsT[j * CAPP + c];
-              const uint32_t bb = sBR[j] & below;
-              pin |= r & (sP[j] & ~bb);
-              xin |= r & (sXP[j] | bb);
+            for (unsigned um = umask[q]; um;) {
+              int jj[RB];
+              uint32_t rr[RB];
+#pragma unroll
+              for (int u = 0; u < RB; ++u) {
+                jj[u] = um ? q * 32 + __ffs(um) - 1 : -1;
+                um &= um - 1;
+              }
+#pragma unroll
+              for (int u = 0; u < RB; ++u) rr[u] = jj[u] < 0 ? 0u : rowsT[jj[u] * CAPP + c];
+#pragma unroll
+              for (int u = 0; u < RB; ++u) {
+                const int j = jj[u];
+                if (j < 0) continue;
+                const uint32_t below = j < w ? 0xffffffffu : (j == w ? (1u << lane) - 1u : 0u);
+                const uint32_t bb = sBR[j] & below;
+                pin |= rr[u] & (sP[j] & ~bb);
+                xin |= rr[u] & (sXP[j] | bb);
+              }
             }
           }
           leaf = pin == 0;
@@ -1114,9 +1140,17 @@ struct Worker {
     const int heavy = a.roots_mode == 1 ? (int)(r_enc >> ROOT_ID_BITS) : 0;
     root_x = a.roots_mode == 1 ? a.col + a.ro[r] : a.xlist + (size_t)owner * a.xcap;
     if (ROWS_SMEM) {
+      // only the rows of the branch's candidates (P | X_P) are ever read below
+      // this node: copy those (lane per candidate), and the member list
       const uint32_t* pb = a.pub + (size_t)owner * (W * CAPP + CAP);
-      for (int w = 0; w < W; ++w)
-        for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = pb[w * CAPP + c];
+      const uint32_t* mbits = a.mbits + (size_t)wid * 2 * W;
+      for (int k = 0; k < W; ++k) {
+        const uint32_t cw = mbits[k] | mbits[W + k];  // broadcast read
+        if ((cw >> lane) & 1u) {
+          const int c = k * 32 + lane;
+          for (int w = 0; w < W; ++w) rowsT[w * CAPP + c] = pb[w * CAPP + c];
+        }
+      }
       for (int c = lane; c < np; c += 32) plist[c] = (int32_t)pb[W * CAPP + c];
     } else {
       rowsT = a.rows_g + (size_t)owner * W * CAPP;
@@ -1526,7 +1560,10 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   int64_t workers = requested_workers > 0 ? requested_workers : resident;
   workers = std::min<int64_t>(workers, resident);
   workers = std::min<int64_t>(workers, by_mem);
-  if (requested_workers <= 0) workers = std::min<int64_t>(workers, std::max<int64_t>(args.num_roots, 1) + resident / 4);
+  // a few narrow roots need few workers; wide roots (deep subtrees) feed every
+  // resident warp through donations, however few they are
+  if (requested_workers <= 0 && W < 8)
+    workers = std::min<int64_t>(workers, std::max<int64_t>(args.num_roots, 1) + resident / 4);
   workers = std::max<int64_t>(workers, 1);
   args.num_workers = (int)workers;
   args.levels = (int)levels;

@@ -26,8 +26,12 @@
  *   -3  device limits (a kernel variant does not fit)
  *   -4  capacity exceeded (reference: induced.CapacityError)
  *
- * Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  All
- * calls are synchronous with respect to the host on return.
+ * Streams: `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Graph-building calls (from_edges / from_text / from_csr / reorder /
+ * preprocess with a NULL degeneracy) return once their work is queued: the
+ * graph is usable on the same stream at once, and its statistics are fetched
+ * asynchronously (mce_graph_info waits for them).  mce_enumerate,
+ * mce_degeneracy_order and mce_graph_copy_csr are synchronous on return.
  */
 #ifndef MCE_B200_H
 #define MCE_B200_H
@@ -80,7 +84,11 @@ void mce_graph_free(mce_graph* g);
  *   method 1: the reference's exact order (minimum current degree, ties to the
  *             smallest id) -- bit-identical positions, single-CTA kernel;
  *   method 0: parallel bucket peeling -- a valid degeneracy order with the same
- *             degeneracy, vertices of one peel round ranked by id. */
+ *             degeneracy, vertices of one peel round ranked by id;
+ *   method 2: asynchronous peeling -- no rounds inside a level: a vertex takes
+ *             its position the moment a decrement brings it to the level; a
+ *             valid degeneracy order with the same degeneracy whose tie-breaks
+ *             vary from run to run (the throughput default of the Python API). */
 int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
                          int position_on_device, int64_t* degeneracy, void* stream);
 
@@ -92,13 +100,17 @@ int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_dev
 /* degeneracy_order + reorder in one call, positions kept on the device
  * (graph.py:239-243 preprocess, minus stats which mce_graph_info gives).
  * The permutation is recoverable from the result's labels:
- * labels[position[v]] = label(v). */
+ * labels[position[v]] = label(v).  `degeneracy` may be NULL: the call then
+ * returns without waiting for the device (the result's max later degree,
+ * from mce_graph_info, is the degeneracy). */
 int mce_preprocess(const mce_graph* g, int method, int64_t* degeneracy, void* stream,
                    mce_graph** out);
 
 typedef struct {
   int roots;             /* 1 = first-level (per vertex), 2 = second-level (per edge) */
-  int induced_full;      /* 1 = full ("ipx"), 0 = partial ("ip") */
+  int induced_full;      /* 1 = full ("ipx"), 0 = partial ("ip"), -1 = auto: partial iff
+                            max_degree / degeneracy > 200 (scheduler.py:36-41), decided on
+                            the device-side graph statistics */
   int workers;           /* worker warps; 0 = every co-resident warp */
   int worker_list;       /* donation protocol on/off (RunConfig.worker_list) */
   int donation_min_p;    /* RunConfig.donation_min_p */
@@ -131,6 +143,7 @@ typedef struct {
   double kernel_ms;      /* device time of the enumeration kernels (CUDA events) */
   int64_t build_bytes;   /* algorithmic graph bytes the induced-subgraph builds read */
   int64_t hist[MCE_HIST_MAX]; /* hist[s] = maximal cliques of size s */
+  int64_t induced_full;  /* the induced mode the run used (resolves auto) */
 } mce_run_result;
 
 /* Enumerate every maximal clique of a canonical, degeneracy-reordered graph

@@ -58,6 +58,7 @@ class RunResultC(ctypes.Structure):
         ("kernel_ms", ctypes.c_double),
         ("build_bytes", ctypes.c_int64),
         ("hist", ctypes.c_int64 * HIST_MAX),
+        ("induced_full", ctypes.c_int64),
     ]
 
 

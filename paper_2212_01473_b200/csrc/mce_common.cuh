@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #define MCE_CHECK(call)                                                          \
   do {                                                                           \
     cudaError_t _e = (call);                                                     \
@@ -37,13 +39,23 @@ struct mce_graph {
   int32_t* col = nullptr;     // nnz
   int64_t* split = nullptr;   // n (lazily built)
   int64_t* labels = nullptr;  // optional: original label of every vertex (set by reorder)
+  // statistics (valid after mce_graph_sync_stats): computed by the split
+  // kernel and copied to pinned host memory asynchronously, so building a
+  // graph never waits for the device
   int64_t max_degree = 0;
   int64_t max_later = 0;      // max |N+(v)|  (= degeneracy on a reordered graph)
   int64_t max_earlier = 0;    // max |N-(v)|
   int device = 0;
+  unsigned long long* stats_dev = nullptr;  // 3 words
+  void* stats_slot = nullptr;               // pinned host words + completion event
+  bool stats_pending = false;
+  uint64_t* vhash = nullptr;  // mix64(label or id) per vertex, built by the first enumeration
+  int vhash_labels = -1;      // which of the two it holds (-1: not built)
 };
 
 int mce_graph_build_split(mce_graph* g, cudaStream_t s);
+// wait (on the graph's own event only) for its statistics
+int mce_graph_sync_stats(const mce_graph* g);
 
 // Keep freed stream-ordered allocations in the device pool (repeated runs
 // reuse HBM instead of returning it to the driver at every synchronisation).
@@ -77,8 +89,7 @@ class Scratch {
   int dev_ = 0;
   bool owner_ = false, synced_ = false;
   size_t used_ = 0, demand_ = 0;
-  void* extra_[64];
-  int nextra_ = 0;
+  std::vector<void*> extra_;
 };
 
 // Free device memory, cached per device for up to a second: cudaMemGetInfo

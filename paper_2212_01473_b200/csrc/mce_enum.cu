@@ -1573,11 +1573,22 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   if (get(&args.stack, (size_t)workers * levels * 4 * W) || get(&args.lpx, (size_t)workers * levels) ||
       get(&args.rpath, (size_t)workers * (levels + 2)) || get(&args.hsum, (size_t)workers * (levels + 2)) ||
       get(&args.xx, (size_t)workers * xcap) || get(&args.xtmp, (size_t)workers * xcap) ||
-      get(&args.mbox, (size_t)workers) || get(&args.mbits, (size_t)workers * 2 * W) ||
-      get(&args.idle_bits, (size_t)(workers + 31) / 32) ||
-      get(&args.wl_wake, (size_t)workers) || get(&args.wl, 1) ||
-      get(&args.root_counter, ROOT_STRIPES * ROOT_STRIDE))
+      get(&args.mbits, (size_t)workers * 2 * W))
     return -1;
+  // the worker list's zero-initialised state in one block, one memset
+  const size_t z_mbox = sizeof(Mailbox) * (size_t)workers;
+  const size_t z_root = sizeof(unsigned long long) * ROOT_STRIPES * ROOT_STRIDE;
+  const size_t z_wl = 128;
+  const size_t z_wake = (sizeof(int) * (size_t)workers + 127) / 128 * 128;
+  const size_t z_idle = (sizeof(unsigned) * (size_t)((workers + 31) / 32) + 127) / 128 * 128;
+  const size_t z_total = z_mbox + z_root + z_wl + z_wake + z_idle;
+  unsigned char* zblk = nullptr;
+  if (get(&zblk, z_total)) return -1;
+  args.root_counter = reinterpret_cast<unsigned long long*>(zblk);
+  args.wl = reinterpret_cast<WorkerListDev*>(zblk + z_root);
+  args.wl_wake = reinterpret_cast<int*>(zblk + z_root + z_wl);
+  args.idle_bits = reinterpret_cast<unsigned*>(zblk + z_root + z_wl + z_wake);
+  args.mbox = reinterpret_cast<Mailbox*>(zblk + z_root + z_wl + z_wake + z_idle);
   args.xrows = nullptr;
   args.xlist = nullptr;
   args.rows_g = nullptr;
@@ -1591,12 +1602,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
                      get(&args.plist_g, (size_t)workers * CAP)))
     return -1;
   if (g_tr) g_tr->mark("class buffers");
-  MCE_CHECK(cudaMemsetAsync(args.wl, 0, sizeof(WorkerListDev), s));
-  MCE_CHECK(cudaMemsetAsync(args.wl_wake, 0, sizeof(int) * workers, s));
-  MCE_CHECK(cudaMemsetAsync(args.idle_bits, 0, sizeof(unsigned) * ((workers + 31) / 32), s));
-  MCE_CHECK(cudaMemsetAsync(args.mbox, 0, sizeof(Mailbox) * workers, s));
-  MCE_CHECK(cudaMemsetAsync(args.root_counter, 0,
-                            sizeof(unsigned long long) * ROOT_STRIPES * ROOT_STRIDE, s));
+  MCE_CHECK(cudaMemsetAsync(zblk, 0, z_total, s));
   const int grid = (int)((workers + WARPS - 1) / WARPS);
   if (g_tr) g_tr->mark("class memsets");
   MCE_CHECK(cudaEventRecord(ev[0], s));
@@ -1689,19 +1695,37 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t stride = cfg->root_stride > 0 ? cfg->root_stride : 1;
   int64_t count = end > begin ? (end - begin + stride - 1) / stride : 0;
 
-  uint64_t* vhash = nullptr;
-  unsigned long long *acc = nullptr, *hist = nullptr, *collect_len = nullptr;
-  long long* wmet = nullptr;
-  int64_t* d_collect = nullptr;
-  if (get(&vhash, n) || get(&acc, 8) || get(&hist, HIST_MAX) || get(&collect_len, 1)) {
-    cleanup();
-    return -1;
+  // per-vertex hash terms: built once per graph (and labelling choice)
+  mce_graph* gm = const_cast<mce_graph*>(g);
+  const int want_labels = (cfg->hash_labels && g->labels) ? 1 : 0;
+  if (gm->vhash_labels != want_labels) {
+    if (!gm->vhash && dalloc(&gm->vhash, n, s)) return -1;
+    k_vhash<<<grid_for(n), 256, 0, s>>>(want_labels ? g->labels : nullptr, n, gm->vhash);
+    mce_count_launch();
+    gm->vhash_labels = want_labels;
   }
-  k_vhash<<<grid_for(n), 256, 0, s>>>(cfg->hash_labels ? g->labels : nullptr, n, vhash);
-  mce_count_launch();
-  MCE_CHECK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), s));
-  MCE_CHECK(cudaMemsetAsync(hist, 0, HIST_MAX * sizeof(unsigned long long), s));
-  MCE_CHECK(cudaMemsetAsync(collect_len, 0, sizeof(unsigned long long), s));
+  const uint64_t* vhash = g->vhash;
+  int64_t metric_slots = 0;
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    metric_slots = cfg->workers > 0 ? cfg->workers : (int64_t)sms * 64;
+  }
+  // every zero-initialised word of the call in one block, one memset:
+  // acc[8] | hist[HIST_MAX] | collect_len | build bytes | root classes + heavy
+  // plan counters [16] | per-worker metrics [4 * metric_slots]
+  constexpr int ZB_CLS = 8 + HIST_MAX + 2;
+  const size_t zwords = (size_t)ZB_CLS + 16 + 4 * (size_t)metric_slots;
+  unsigned long long* zb = nullptr;
+  if (get(&zb, zwords)) return -1;
+  MCE_CHECK(cudaMemsetAsync(zb, 0, zwords * sizeof(unsigned long long), s));
+  unsigned long long* acc = zb;
+  unsigned long long* hist = zb + 8;
+  unsigned long long* collect_len = zb + 8 + HIST_MAX;
+  unsigned long long* bb = collect_len + 1;
+  long long* wmet = reinterpret_cast<long long*>(zb + ZB_CLS + 16);
+  int64_t* d_collect = nullptr;
   if (cfg->collect_cap > 0 && get(&d_collect, cfg->collect_cap)) {
     cleanup();
     return -1;
@@ -1711,9 +1735,6 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t launches = 0;
   int64_t trivial_nodes = 0;
   int64_t workers_used = 0;
-  unsigned long long* bb = nullptr;
-  if (get(&bb, 1)) return -1;
-  MCE_CHECK(cudaMemsetAsync(bb, 0, sizeof(unsigned long long), s));
   // timing events, created once per device (one call at a time uses them: the
   // call holds them until its final synchronisation)
   static cudaEvent_t ev_cache[64][2 * NUM_WIDTHS];
@@ -1733,14 +1754,13 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   if (count > 0) {
     uint32_t *keys = nullptr, *keys2 = nullptr;
     int64_t *roots = nullptr, *roots2 = nullptr;
-    unsigned long long* cls = nullptr;
+    unsigned long long* cls = zb + ZB_CLS;  // zeroed above
     constexpr int HMETA = MAXP_SLOT + 1;  // cls[HMETA .. HMETA+2] = heavy plan counters
-    if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count) ||
-        get(&cls, HMETA + 3)) {
+    static_assert(HMETA + 3 <= 16, "class/heavy counters exceed their zeroed slots");
+    if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count)) {
       cleanup();
       return -1;
     }
-    MCE_CHECK(cudaMemsetAsync(cls, 0, (HMETA + 3) * sizeof(unsigned long long), s));
     HeavyPlan hp{};
     // device memory this call may use: free HBM plus the scratch arena it holds
     size_t avail_b = 0;
@@ -1749,7 +1769,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     {
       const size_t free_b = avail_b;
       const char* e = getenv("MCE_HEAVY");  // diagnostics: MCE_HEAVY=0 disables the pre-pass
-      hp.enabled = cfg->roots == 1 && !(e && atoi(e) == 0) && g->max_earlier >= HEAVY_X_MIN;
+      hp.enabled = cfg->roots == 1 && !(e && atoi(e) == 0);
       hp.pool_cap = std::min<unsigned long long>(free_b / 16, 1ull << 30) / sizeof(uint32_t);
       hp.meta = cls + HMETA;
       if (hp.enabled && (get(&hp.vertex, HEAVY_MAX) || get(&hp.off, HEAVY_MAX) ||
@@ -1776,6 +1796,14 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     tr.mark("root keys+sort queued");
     MCE_CHECK(cudaStreamSynchronize(s));
     tr.mark("class counts synced");
+    if (mce_graph_sync_stats(g)) return -1;  // complete by now (the stream is idle)
+    // induced = auto: the reference's rule (scheduler.py:36-41) on the reordered
+    // graph, whose max |N+(v)| is the degeneracy
+    const bool full = cfg->induced_full >= 0
+                          ? cfg->induced_full != 0
+                          : !(g->max_later > 0 &&
+                              (double)g->max_degree / (double)g->max_later > 200.0);
+    out->induced_full = full ? 1 : 0;
     const int64_t* sorted_roots = dv.Current();
     // heavy-X roots: their X rows over the whole grid, before the enumeration
     uint32_t* heavy_pool = nullptr;
@@ -1820,19 +1848,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     int64_t wcap = 0;
     double frac = cfg->mem_fraction > 0 ? cfg->mem_fraction : 0.5;
     size_t budget = (size_t)(avail_b * frac);
-    // per-worker metrics accumulate across class launches
-    int64_t metric_slots = 0;
-    {
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      metric_slots = cfg->workers > 0 ? cfg->workers : (int64_t)sms * 64;
-    }
-    if (get(&wmet, metric_slots * 4)) {
-      cleanup();
-      return -1;
-    }
-    MCE_CHECK(cudaMemsetAsync(wmet, 0, sizeof(long long) * 4 * metric_slots, s));
+    // per-worker metrics (zeroed above) accumulate across class launches
     for (const ClassPlan& cp : plan) {
       EnumArgs args{};
       args.n = n;
@@ -1867,7 +1883,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       cudaEvent_t* ev = &events[2 * nev++];
       bool xr = false;
       const int xmin = cfg->partial_xrows_min_w > 0 ? cfg->partial_xrows_min_w : 1;
-      int rc = launch_mode(cfg->induced_full != 0, cp.W, xmin, args, req, &workers_used, s,
+      int rc = launch_mode(full, cp.W, xmin, args, req, &workers_used, s,
                            &launches, budget, guess, ev, &xr, scr);
       tr.mark("class launched");
       if (rc) {
@@ -1908,6 +1924,13 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       trivial_nodes = trivial_count;  // one visited node each (scheduler.py:300-301)
     }
     (void)wcap;
+  }
+  if (count <= 0) {  // no roots: still report the induced mode an auto run resolves to
+    if (mce_graph_sync_stats(g)) return -1;
+    out->induced_full = cfg->induced_full >= 0
+                            ? (cfg->induced_full != 0)
+                            : !(g->max_later > 0 &&
+                                (double)g->max_degree / (double)g->max_later > 200.0);
   }
   if (cfg->roots == 2 && cfg->include_isolated) {
     int64_t* all = nullptr;

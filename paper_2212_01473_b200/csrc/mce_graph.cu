@@ -115,18 +115,14 @@ int Scratch::raw(void** p, size_t bytes) {
       return 0;
     }
   }
-  if (nextra_ >= 64) {
-    mce_set_error("scratch: too many overflow allocations");
-    return -1;
-  }
   MCE_CHECK(cudaMallocAsync(p, bytes, s_));
-  extra_[nextra_++] = *p;
+  extra_.push_back(*p);
   return 0;
 }
 
 Scratch::~Scratch() {
   if (!synced_) cudaStreamSynchronize(s_);
-  for (int i = 0; i < nextra_; ++i) cudaFreeAsync(extra_[i], s_);
+  for (void* q : extra_) cudaFreeAsync(q, s_);
   if (owner_) {
     ArenaState& a = g_arena[dev_];
     std::lock_guard<std::mutex> lk(a.mu);
@@ -989,21 +985,77 @@ int order_device(const mce_graph* g, int method, int64_t* d_pos, int64_t* d_deg,
 
 }  // namespace
 
+namespace {
+// Pinned host words + an event per graph for its statistics, recycled.
+struct StatsSlot {
+  unsigned long long* host;
+  cudaEvent_t ev;
+  int dev;
+};
+std::mutex g_slot_mu;
+std::vector<StatsSlot*> g_free_slots[64];
+
+StatsSlot* stats_slot_get(int dev) {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  auto& fl = g_free_slots[dev];
+  if (fl.empty()) {
+    constexpr int BATCH = 256;
+    unsigned long long* block = nullptr;
+    if (cudaHostAlloc((void**)&block, BATCH * 4 * sizeof(unsigned long long), cudaHostAllocPortable) !=
+        cudaSuccess)
+      return nullptr;
+    for (int i = 0; i < BATCH; ++i) {
+      StatsSlot* sl = new StatsSlot{block + 4 * i, nullptr, dev};
+      if (cudaEventCreateWithFlags(&sl->ev, cudaEventDisableTiming) != cudaSuccess) {
+        delete sl;
+        return nullptr;
+      }
+      fl.push_back(sl);
+    }
+  }
+  StatsSlot* sl = fl.back();
+  fl.pop_back();
+  return sl;
+}
+
+void stats_slot_put(StatsSlot* sl) {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_free_slots[sl->dev].push_back(sl);
+}
+}  // namespace
+
 int mce_graph_build_split(mce_graph* g, cudaStream_t s) {
   if (!g->split && dev_alloc(&g->split, g->n, s)) return -1;
-  unsigned long long* st = nullptr;
-  if (dev_alloc(&st, 3, s)) return -1;
-  MCE_CHECK(cudaMemsetAsync(st, 0, 3 * sizeof(unsigned long long), s));
-  if (g->n > 0) k_split<<<grid_for(g->n), 256, 0, s>>>(g->ro, g->col, g->n, g->split, st);
+  if (!g->stats_dev && dev_alloc(&g->stats_dev, 3, s)) return -1;
+  MCE_CHECK(cudaMemsetAsync(g->stats_dev, 0, 3 * sizeof(unsigned long long), s));
+  if (g->n > 0) k_split<<<grid_for(g->n), 256, 0, s>>>(g->ro, g->col, g->n, g->split, g->stats_dev);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
-  unsigned long long h[3];
-  MCE_CHECK(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
-  MCE_CHECK(cudaStreamSynchronize(s));
-  dev_free(st, s);
-  g->max_degree = (int64_t)h[0];
-  g->max_later = (int64_t)h[1];
-  g->max_earlier = (int64_t)h[2];
+  StatsSlot* sl = static_cast<StatsSlot*>(g->stats_slot);
+  if (!sl) {
+    sl = stats_slot_get(g->device >= 0 && g->device < 64 ? g->device : 0);
+    if (!sl) {
+      mce_set_error("pinned statistics slot allocation failed");
+      return -1;
+    }
+    g->stats_slot = sl;
+  }
+  MCE_CHECK(cudaMemcpyAsync(sl->host, g->stats_dev, 3 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaEventRecord(sl->ev, s));
+  g->stats_pending = true;
+  return 0;
+}
+
+int mce_graph_sync_stats(const mce_graph* cg) {
+  mce_graph* g = const_cast<mce_graph*>(cg);
+  if (!g->stats_pending) return 0;
+  StatsSlot* sl = static_cast<StatsSlot*>(g->stats_slot);
+  MCE_CHECK(cudaEventSynchronize(sl->ev));
+  g->max_degree = (int64_t)sl->host[0];
+  g->max_later = (int64_t)sl->host[1];
+  g->max_earlier = (int64_t)sl->host[2];
+  g->stats_pending = false;
   return 0;
 }
 
@@ -1123,6 +1175,7 @@ extern "C" {
 int mce_graph_info(const mce_graph* g, int64_t* n, int64_t* nnz, int64_t* max_degree,
                    int64_t* max_later, int64_t* max_earlier) {
   if (!g) { mce_set_error("null graph"); return -2; }
+  if (mce_graph_sync_stats(g)) return -1;
   if (n) *n = g->n;
   if (nnz) *nnz = g->nnz;
   if (max_degree) *max_degree = g->max_degree;
@@ -1165,6 +1218,13 @@ void mce_graph_free(mce_graph* g) {
   if (g->col) cudaFreeAsync(g->col, 0);
   if (g->split) cudaFreeAsync(g->split, 0);
   if (g->labels) cudaFreeAsync(g->labels, 0);
+  if (g->stats_dev) cudaFreeAsync(g->stats_dev, 0);
+  if (g->vhash) cudaFreeAsync(g->vhash, 0);
+  if (g->stats_slot) {
+    StatsSlot* sl = static_cast<StatsSlot*>(g->stats_slot);
+    cudaEventSynchronize(sl->ev);  // its copy must land before the slot is reused
+    stats_slot_put(sl);
+  }
   if (cur != g->device) cudaSetDevice(cur);
   delete g;
 }
@@ -1262,14 +1322,16 @@ int mce_preprocess(const mce_graph* g, int method, int64_t* degeneracy, void* st
   mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   *out = nullptr;
-  *degeneracy = 0;
+  if (degeneracy) *degeneracy = 0;
   if (g->n == 0) return mce_reorder(g, nullptr, 1, stream, out);
   int64_t* d_pos = nullptr;
   int64_t* d_deg = nullptr;
   if (dev_alloc(&d_pos, g->n, s) || dev_alloc(&d_deg, 1, s)) return -1;
   int rc = order_device(g, method, d_pos, d_deg, s);
   if (!rc) rc = mce_reorder(g, d_pos, 1, stream, out);  // ends with a stream sync
-  if (!rc) MCE_CHECK(cudaMemcpy(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  // NULL degeneracy: no wait (the reordered graph's max |N+(v)| is the degeneracy,
+  // available through mce_graph_info)
+  if (!rc && degeneracy) MCE_CHECK(cudaMemcpy(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost));
   dev_free(d_pos, s);
   dev_free(d_deg, s);
   return rc;

@@ -32,7 +32,6 @@ sizes differ.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
 from typing import IO, Iterable
 
 import numpy as np
@@ -199,14 +198,55 @@ class Graph:
         return f"Graph(num_vertices={self.num_vertices}, num_edges={self.num_edges})"
 
 
-@dataclass(frozen=True)
 class GraphStats:
-    """Headline numbers: size, max degree, degeneracy (reference graph.py:86-92)."""
+    """Headline numbers: size, max degree, degeneracy (reference graph.py:86-92).
 
-    n: int
-    m: int
-    max_degree: int
-    degeneracy: int
+    ``max_degree`` / ``degeneracy`` may be resolved lazily (``preprocess``
+    returns before the device has finished: they are read from the device
+    graph's statistics on first access)."""
+
+    __slots__ = ("n", "_m", "_max_degree", "_degeneracy", "_thunk")
+
+    def __init__(self, n: int, m: int | None = None, max_degree: int | None = None,
+                 degeneracy: int | None = None, _thunk=None) -> None:
+        self.n = int(n)
+        self._m = m
+        self._max_degree = max_degree
+        self._degeneracy = degeneracy
+        self._thunk = _thunk
+
+    def _resolve(self) -> None:
+        m, md, d = self._thunk()
+        self._m = int(m) if self._m is None else self._m
+        self._max_degree = int(md) if self._max_degree is None else self._max_degree
+        self._degeneracy = int(d) if self._degeneracy is None else self._degeneracy
+        self._thunk = None
+
+    @property
+    def m(self) -> int:
+        if self._m is None:
+            self._resolve()
+        return self._m
+
+    @property
+    def max_degree(self) -> int:
+        if self._max_degree is None:
+            self._resolve()
+        return self._max_degree
+
+    @property
+    def degeneracy(self) -> int:
+        if self._degeneracy is None:
+            self._resolve()
+        return self._degeneracy
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, GraphStats) and (self.n, self.m, self.max_degree, self.degeneracy) \
+            == (other.n, other.m, other.max_degree, other.degeneracy)
+
+    def __repr__(self) -> str:
+        return (f"GraphStats(n={self.n}, m={self.m}, max_degree={self.max_degree}, "
+                f"degeneracy={self.degeneracy})")
 
 
 class DegeneracyOrder:
@@ -214,12 +254,21 @@ class DegeneracyOrder:
     (reference graph.py:96-100).  ``position`` may be produced lazily (by
     ``preprocess``, which keeps the permutation on the device)."""
 
-    __slots__ = ("_position", "degeneracy", "_thunk")
+    __slots__ = ("_position", "_degeneracy", "_thunk", "_dthunk")
 
-    def __init__(self, position: np.ndarray | None, degeneracy: int, _thunk=None) -> None:
+    def __init__(self, position: np.ndarray | None, degeneracy: int | None, _thunk=None,
+                 _dthunk=None) -> None:
         self._position = position
-        self.degeneracy = int(degeneracy)
+        self._degeneracy = None if degeneracy is None else int(degeneracy)
         self._thunk = _thunk
+        self._dthunk = _dthunk
+
+    @property
+    def degeneracy(self) -> int:
+        if self._degeneracy is None:
+            self._degeneracy = int(self._dthunk())
+            self._dthunk = None
+        return self._degeneracy
 
     @property
     def position(self) -> np.ndarray:
@@ -361,9 +410,10 @@ def preprocess(g: Graph, method: str = "async") -> tuple[Graph, DegeneracyOrder,
         order = DegeneracyOrder(np.empty(0, dtype=np.int64), 0)
         g2 = from_edges(np.empty((0, 2), dtype=np.int64), 0)
         return g2, order, stats(g2, order)
-    d = ctypes.c_int64(0)
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib().mce_preprocess(g.device.handle, ORDER_METHODS[method], ctypes.byref(d),
+    # no degeneracy out-parameter: the call returns once its work is queued;
+    # the reordered graph's max later degree is the degeneracy
+    _lib.check(_lib.lib().mce_preprocess(g.device.handle, ORDER_METHODS[method], None,
                                          None, ctypes.byref(h)), "mce_preprocess")
     g2 = Graph(n, _device=_DeviceGraph(h), _device_labels=True)
     base = g.labels
@@ -374,5 +424,10 @@ def preprocess(g: Graph, method: str = "async") -> tuple[Graph, DegeneracyOrder,
         inv[g2.labels] = np.arange(n, dtype=np.int64)
         return inv if base is None else inv[base]
 
-    order = DegeneracyOrder(None, int(d.value), _thunk=position)
-    return g2, order, stats(g2, order)
+    def device_stats() -> tuple[int, int, int]:
+        info = g2.device_info()
+        return info["nnz"] // 2, info["max_degree"], info["max_later"]
+
+    order = DegeneracyOrder(None, None, _thunk=position, _dthunk=lambda: device_stats()[2])
+    st = GraphStats(n, _thunk=device_stats)
+    return g2, order, st

@@ -168,11 +168,13 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
     cfg.validate()
     if sink is None:
         sink = CliqueSink(collect_limit=cfg.collect_limit)
+    # "auto" is resolved on the device side (the same rule, choose_induced_mode,
+    # on the graph's device statistics) so that the call does not wait for them
     induced = cfg.induced
-    if induced == "auto":
-        induced = choose_induced_mode(st.max_degree, st.degeneracy)
     limit = sink.collect_limit
     if g.num_vertices == 0:
+        if induced == "auto":
+            induced = choose_induced_mode(st.max_degree, st.degeneracy)
         return RunResult(0, 0, cfg.roots, induced, cfg.resolved_workers(), 0.0, 0.0, 0.0,
                          [WorkerMetrics(worker_id=0, enabled=cfg.timing)], timing=cfg.timing)
     _lib.require_device()
@@ -183,7 +185,7 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
     while True:
         c = _lib.RunConfigC(
             roots=1 if cfg.roots == "l1" else 2,
-            induced_full=1 if induced == "ipx" else 0,
+            induced_full={"ipx": 1, "ip": 0, "auto": -1}[induced],
             workers=int(cfg.workers),
             worker_list=int(bool(cfg.worker_list)),
             donation_min_p=int(cfg.donation_min_p),
@@ -218,6 +220,7 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
         if room > 0:
             sink.collected.extend(got[:room])
     sink.total += int(res.cliques)
+    induced = "ipx" if int(res.induced_full) else "ip"
     workers = max(int(res.workers), 1)
     hist_arr = np.ctypeslib.as_array(res.hist)
     hist = {int(s): int(hist_arr[s]) for s in np.flatnonzero(hist_arr)}

@@ -217,3 +217,24 @@ def test_async_peel_on_reference_graphs():
         exp = case["runs"]["l1-ipx"]
         assert res.clique_count == exp["count"], case["name"]
         assert res.clique_hash_hex == exp["hash"], case["name"]
+
+
+def test_every_width_class_in_one_call():
+    """Disjoint cliques whose first-level roots fall in seven bitset classes
+    (|P| up to 1049 -> W = 1 ... 64): one call launches every class (the
+    first call of a process takes its scratch from the pool), and each
+    clique is exactly one maximal clique."""
+    sizes = [5, 40, 70, 140, 270, 530, 1050]
+    parts, base = [], 0
+    for s in sizes:
+        u, v = np.triu_indices(s, k=1)
+        parts.append(np.column_stack((u + base, v + base)))
+        base += s
+    g = from_edges(np.concatenate(parts).astype(np.int64), base)
+    g2, _, st = preprocess(g)
+    assert st.degeneracy == max(sizes) - 1
+    for induced in ("ipx", "ip"):
+        res = run(g2, st, RunConfig(induced=induced))
+        assert res.clique_count == len(sizes)
+        assert res.size_histogram == {s: 1 for s in sizes}
+        assert res.kernel_launches >= 7

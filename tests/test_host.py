@@ -152,3 +152,22 @@ def test_run_result_lazy_worker_metrics():
     assert [w.donations_made for w in wm] == [0, 1]
     assert res.report().nodes_total == 12 and res.report().load_ratio == pytest.approx(7 / 6)
     assert res.worker_metrics is wm
+
+
+def test_graph_stats_lazy_resolution():
+    """preprocess returns before the device finishes: GraphStats resolves its
+    fields from the device statistics on first access, once."""
+    from paper_2212_01473_b200.graph import GraphStats
+
+    calls = []
+
+    def thunk():
+        calls.append(1)
+        return 10, 7, 3
+
+    st = GraphStats(5, _thunk=thunk)
+    assert st.n == 5 and calls == []
+    assert (st.m, st.max_degree, st.degeneracy) == (10, 7, 3)
+    assert calls == [1]
+    assert st == GraphStats(5, 10, 7, 3)
+    assert "degeneracy=3" in repr(st)

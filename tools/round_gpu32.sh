@@ -1,0 +1,4 @@
+out=gpurun_out
+timeout -s KILL 900 python -m pytest tests -m gpu -q -x > $out/pytest_gpu_r1z.log 2>&1; echo "pytest rc=$?"; tail -3 $out/pytest_gpu_r1z.log
+timeout -s KILL 120 python tools/host_trace.py ba200k 2>/dev/null | head -5
+timeout -s KILL 300 python bench.py --no-cpu-baseline > $out/bench_ba200k_r1z.json 2> $out/bench_ba200k_r1z.err; cat $out/bench_ba200k_r1z.json; tail -1 $out/bench_ba200k_r1z.err

@@ -452,8 +452,8 @@ k_peel_persistent(const int64_t* __restrict__ ro, const int32_t* __restrict__ co
 // task queue of 32-edge chunks by every warp of the grid, and a decrement
 // that takes a neighbour from k+1 to k claims it on the spot (its chunks are
 // appended to the queue).  The level ends at quiescence -- every claimed
-// chunk processed -- detected on ONE packed word (chunks claimed << 32 |
-// chunks done).  Positions are handed out at claim time, so a vertex's later
+// chunk processed -- detected on two monotonic counters (chunks claimed,
+// chunks done; done is read first).  Positions are handed out at claim time, so a vertex's later
 // neighbours are exactly those that had not decremented it yet: at most k,
 // a valid degeneracy order (graph.py:183-210's invariant) with the same
 // degeneracy, in a data-dependent order (tie-breaks differ from run to run).
@@ -501,21 +501,18 @@ __device__ __forceinline__ void agrid_barrier(APeelShared* sh, unsigned int nblo
 // from vclaim, chunk descriptors appended to the queue; `done` processed
 // chunks are retired in the same atomic as the new chunks are claimed (same
 // word: the claims are counted before the work that found them is retired).
+// cand[t]'s adjacency is col[e0[t], e1[t]) (the caller loads the offsets --
+// the consumer ahead of its decrements, off the dependent chain)
 template <int MAXC>
-__device__ __forceinline__ void apeel_claim(const int64_t* __restrict__ ro, const int32_t (&cand)[MAXC],
+__device__ __forceinline__ void apeel_claim(const int32_t (&cand)[MAXC], const int64_t (&e0)[MAXC],
+                                            const int64_t (&e1)[MAXC],
                                             int cnt, unsigned done, APeelShared* sh,
                                             uint64_t* __restrict__ tasks, int32_t* __restrict__ order,
                                             uint8_t* __restrict__ removed, int lane) {
   int nch = 0;
-  int64_t e0[MAXC];
 #pragma unroll
-  for (int t = 0; t < MAXC; ++t) {
-    if (t < cnt) {
-      const int32_t v = cand[t];
-      e0[t] = ro[v];
-      nch += (int)((ro[v + 1] - e0[t] + 31) >> 5);
-    }
-  }
+  for (int t = 0; t < MAXC; ++t)
+    if (t < cnt) nch += (int)((e1[t] - e0[t] + 31) >> 5);
   int ic = cnt, in = nch;  // inclusive warp scans of vertices and chunks
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -552,9 +549,9 @@ __device__ __forceinline__ void apeel_claim(const int64_t* __restrict__ ro, cons
       const int32_t v = cand[t];
       order[vp++] = v;
       removed[v] = 1;
-      const int64_t e1 = ro[v + 1];
-      for (int64_t st = e0[t]; st < e1; st += 32) {
-        const int64_t len = e1 - st < 32 ? e1 - st : 32;
+      const int64_t end = e1[t];
+      for (int64_t st = e0[t]; st < end; st += 32) {
+        const int64_t len = end - st < 32 ? end - st : 32;
         tasks[tp++] = ((uint64_t)st << 6) | (uint64_t)len;
       }
     }
@@ -610,7 +607,8 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
       if (tm) {
         if (lane == 0) atomicAdd(&sh->scan_claims, (unsigned)__popc(tm));
         int32_t c1[1] = {v};
-        apeel_claim<1>(ro, c1, take ? 1 : 0, 0u, sh, tasks, order, removed, lane);
+        int64_t a1[1] = {take ? ro[v] : 0}, b1[1] = {take ? ro[v + 1] : 0};
+        apeel_claim<1>(c1, a1, b1, take ? 1 : 0, 0u, sh, tasks, order, removed, lane);
       }
     }
     agrid_barrier(sh, G, nothing);
@@ -664,6 +662,7 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
         if (over) break;
         // c chunks: lane l takes edge l of each; c decrements in flight per lane
         int32_t cand[APEEL_BATCH];
+        int64_t c0[APEEL_BATCH], c1[APEEL_BATCH];
         int cnt = 0;
         int32_t u[APEEL_BATCH];
 #pragma unroll
@@ -672,11 +671,26 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
           u[t] = -1;
           if (t < c && lane < (int)(dt & 63)) u[t] = col[(int64_t)(dt >> 6) + lane];
         }
+        // every neighbour's adjacency range, loaded alongside its decrement
+        // (a crosser's chunks are enqueued without another round trip)
+        int64_t r0[APEEL_BATCH], r1[APEEL_BATCH];
+        int old_deg[APEEL_BATCH];
 #pragma unroll
         for (int t = 0; t < APEEL_BATCH; ++t) {
-          if (u[t] >= 0 && atomicSub(&deg[u[t]], 1) == kp1) cand[cnt++] = u[t];
+          r0[t] = u[t] >= 0 ? __ldg(&ro[u[t]]) : 0;
+          r1[t] = u[t] >= 0 ? __ldg(&ro[u[t] + 1]) : 0;
+          old_deg[t] = u[t] >= 0 ? atomicSub(&deg[u[t]], 1) : 0;
         }
-        apeel_claim<APEEL_BATCH>(ro, cand, cnt, (unsigned)c, sh, tasks, order, removed, lane);
+#pragma unroll
+        for (int t = 0; t < APEEL_BATCH; ++t) {
+          if (u[t] >= 0 && old_deg[t] == kp1) {
+            cand[cnt] = u[t];
+            c0[cnt] = r0[t];
+            c1[cnt] = r1[t];
+            ++cnt;
+          }
+        }
+        apeel_claim<APEEL_BATCH>(cand, c0, c1, cnt, (unsigned)c, sh, tasks, order, removed, lane);
         got += c;
       }
     }

@@ -816,6 +816,72 @@ __global__ void k_scatter_rows(const int64_t* __restrict__ ro, const int32_t* __
   }
 }
 
+// Relabel and sort each row in one pass, one warp per source row: rows of
+// <= 32 entries are sorted in registers (bitonic network over the lanes),
+// rows of <= REORDER_SMEM entries by a bitonic sort in the warp's shared
+// memory; longer rows are written unsorted to `tmp` and listed as segments
+// (begin/end) for one segmented sort afterwards.
+constexpr int REORDER_THREADS = 256;
+constexpr int REORDER_SMEM = 1024;
+__global__ void __launch_bounds__(REORDER_THREADS)
+k_reorder_rows(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+               const int64_t* __restrict__ pos, const int64_t* __restrict__ nro,
+               int32_t* __restrict__ out, int32_t* __restrict__ tmp, int64_t* __restrict__ seg_b,
+               int64_t* __restrict__ seg_e, unsigned long long* __restrict__ nlong) {
+  __shared__ int32_t sbuf[REORDER_THREADS / 32][REORDER_SMEM];
+  const int lane = threadIdx.x & 31;
+  int32_t* buf = sbuf[threadIdx.x >> 5];
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t src = ro[v];
+    const int d = (int)(ro[v + 1] - src);
+    const int64_t dst = nro[pos[v]];
+    if (d <= 32) {
+      int32_t x = lane < d ? (int32_t)pos[col[src + lane]] : 0x7fffffff;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+          const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+          x = (lower == up) ? min(x, y) : max(x, y);
+        }
+      }
+      if (lane < d) out[dst + lane] = x;
+    } else if (d <= REORDER_SMEM) {
+      int p2 = 64;
+      while (p2 < d) p2 <<= 1;
+      for (int i = lane; i < p2; i += 32) buf[i] = i < d ? (int32_t)pos[col[src + i]] : 0x7fffffff;
+      __syncwarp();
+      for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = lane; i < p2; i += 32) {
+            const int ij = i ^ j;
+            if (ij > i) {
+              const int32_t a = buf[i], b = buf[ij];
+              if ((a > b) == ((i & k) == 0)) {
+                buf[i] = b;
+                buf[ij] = a;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int i = lane; i < d; i += 32) out[dst + i] = buf[i];
+      __syncwarp();
+    } else {
+      for (int i = lane; i < d; i += 32) tmp[dst + i] = (int32_t)pos[col[src + i]];
+      if (lane == 0) {
+        const unsigned long long idx = atomicAdd(nlong, 1ull);
+        seg_b[idx] = dst;
+        seg_e[idx] = dst + d;
+      }
+    }
+  }
+}
+
 __global__ void k_relabel(const int64_t* __restrict__ pos, int64_t n,
                           const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -1304,15 +1370,26 @@ int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_dev
     MCE_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, ndeg, h->ro, n + 1, s));
     cudaFreeAsync(tmp, s);
     if (nnz > 0) {
-      k_scatter_rows<<<grid_for(n * 32), 256, 0, s>>>(g->ro, g->col, n, d_pos, h->ro, tmpcol);
+      // rows sorted in place by k_reorder_rows; the few long ones listed as
+      // segments (the rest of the list stays empty) for one segmented sort
+      int64_t* seg = nullptr;
+      unsigned long long* nlong = nullptr;
+      if (dev_alloc(&seg, 2 * n, s) || dev_alloc(&nlong, 1, s)) return -1;
+      MCE_CHECK(cudaMemsetAsync(seg, 0, sizeof(int64_t) * 2 * n, s));
+      MCE_CHECK(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), s));
+      k_reorder_rows<<<grid_for(n * 32, REORDER_THREADS), REORDER_THREADS, 0, s>>>(
+          g->ro, g->col, n, d_pos, h->ro, h->col, tmpcol, seg, seg + n, nlong);
       mce_count_launch();
+      MCE_CHECK(cudaGetLastError());
       tb = 0;
-      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmpcol, h->col, nnz, n, h->ro,
-                                                   h->ro + 1, s));
+      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmpcol, h->col, nnz, n, seg,
+                                                   seg + n, s));
       MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
-      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, tmpcol, h->col, nnz, n, h->ro,
-                                                   h->ro + 1, s));
+      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, tmpcol, h->col, nnz, n, seg,
+                                                   seg + n, s));
       cudaFreeAsync(tmp, s);
+      dev_free(seg, s);
+      dev_free(nlong, s);
     }
     k_relabel<<<grid_for(n), 256, 0, s>>>(d_pos, n, g->labels, h->labels);
     mce_count_launch();

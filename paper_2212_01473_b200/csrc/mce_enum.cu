@@ -379,6 +379,7 @@ struct Worker {
     }
     __syncwarp();
     if (np == 0) return nr;
+    if (W == 1 && lane >= np) plist[lane] = 0x7fffffff;  // padded for find32
     // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i)
     for (int w = 0; w < W; ++w)
       for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
@@ -393,9 +394,9 @@ struct Worker {
           len = (int)(a.ro[ai + 1] - lo);
         },
         [&](int io, int32_t w) {
-          const int j = bsearch_i32(plist + io + 1, np - io - 1, w);
-          if (j >= 0) {
-            const int jj = io + 1 + j;
+          // N+(a_io) holds only vertices after a_io: a hit is past io
+          const int jj = W == 1 ? find32(w) : io + 1 + bsearch_i32(plist + io + 1, np - io - 1, w);
+          if (jj > io) {
             atomicOr(&rowsT[(jj >> 5) * CAPP + io], 1u << (jj & 31));
             atomicOr(&rowsT[(io >> 5) * CAPP + jj], 1u << (io & 31));
           }
@@ -426,12 +427,23 @@ struct Worker {
             len = (int)(a.ro[x + 1] - lo);
           },
           [&](int t, int32_t w) {
-            const int j = bsearch_i32(plist, np, w);
+            const int j = W == 1 ? find32(w) : bsearch_i32(plist, np, w);
             if (j >= 0) atomicOr(&xrowsT[(size_t)(j >> 5) * a.xcap + t], 1u << (j & 31));
           });
     }
     __syncwarp();
     return nr;
+  }
+
+  // W = 1: index of w in the padded 32-entry plist (branchless, 5 steps), -1 if absent
+  __device__ __forceinline__ int find32(int32_t w) const {
+    int i = 0;
+    i += plist[i + 15] < w ? 16 : 0;
+    i += plist[i + 7] < w ? 8 : 0;
+    i += plist[i + 3] < w ? 4 : 0;
+    i += plist[i + 1] < w ? 2 : 0;
+    i += plist[i] < w ? 1 : 0;
+    return plist[i] == w ? i : -1;
   }
 
   // ---------------------------------------------------------------- pieces

@@ -380,57 +380,50 @@ struct Worker {
     __syncwarp();
     if (np == 0) return nr;
     if (W == 1 && lane >= np) plist[lane] = 0x7fffffff;  // padded for find32
-    // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i)
-    for (int w = 0; w < W; ++w)
-      for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
-    __syncwarp();
-    // P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i);
-    // N+(a_i) & P lies after a_i in the ascending plist
-    flat_walk(
-        np,
-        [&](int i, int64_t& lo, int& len) {
-          const int32_t ai = plist[i];
-          lo = a.split[ai];
-          len = (int)(a.ro[ai + 1] - lo);
-        },
-        [&](int io, int32_t w) {
-          // N+(a_io) holds only vertices after a_io: a hit is past io
-          const int jj = W == 1 ? find32(w) : io + 1 + bsearch_i32(plist + io + 1, np - io - 1, w);
-          if (jj > io) {
-            atomicOr(&rowsT[(jj >> 5) * CAPP + io], 1u << (jj & 31));
-            atomicOr(&rowsT[(io >> 5) * CAPP + jj], 1u << (io & 31));
-          }
-        });
     // Partial mode builds X rows only when |X| is moderate: a hub late in the
     // order (|X| in the thousands, tiny P) visits few nodes, and its handful
     // of X_X scans through the CSR cost less than sum |N+(x)| row-building
     // loads.  Full mode always needs them (X_X pivot candidates).
     xr = XROWS && (PIVOT_XX || heavy > 0 || nx <= a.xrows_partial_max);
+    // a heavy-X root's rows were built by the whole grid (k_heavy_xrows)
+    const bool xwalk = xr && heavy == 0;
     if (xr && heavy > 0) {
-      // a heavy-X root's rows were built by the whole grid (k_heavy_xrows)
       xrowsT = const_cast<uint32_t*>(a.heavy_rows) + a.heavy_off[heavy - 1];
       xstride = nx;
-    } else if (xr) {
-      // X rows (induced.py:95-103): X member x is earlier than every P vertex,
-      // so its P-neighbours are N+(x) & P.  Same flattened (member,
-      // neighbour) walk as the P rows: a root with a huge X (a hub late in
-      // the order) costs sum |N+(x)| / 32 independent loads per lane, not a
-      // serial scan per lane.
+    }
+    for (int w = 0; w < W; ++w)
+      for (int c = lane; c < np; c += 32) rowsT[w * CAPP + c] = 0;
+    if (xwalk)
       for (int w = 0; w < W; ++w)
         for (int t = lane; t < nx; t += 32) xrowsT[(size_t)w * a.xcap + t] = 0;
-      __syncwarp();
-      flat_walk(
-          nx,
-          [&](int t, int64_t& lo, int& len) {
-            const int32_t x = root_x[t];
-            lo = a.split[x];
-            len = (int)(a.ro[x + 1] - lo);
-          },
-          [&](int t, int32_t w) {
+    __syncwarp();
+    // One flattened walk over the P members then the X members (a small root
+    // fills one pass instead of two half-empty ones):
+    //  * P rows (induced.py:61-92): each P-P edge (a_i, b) with b in N+(a_i);
+    //    N+(a_i) & P lies after a_i in the ascending plist;
+    //  * X rows (induced.py:95-103): X member x is earlier than every P
+    //    vertex, so its P-neighbours are N+(x) & P.
+    flat_walk(
+        np + (xwalk ? nx : 0),
+        [&](int i, int64_t& lo, int& len) {
+          const int32_t m = i < np ? plist[i] : root_x[i - np];
+          lo = a.split[m];
+          len = (int)(a.ro[m + 1] - lo);
+        },
+        [&](int i, int32_t w) {
+          if (i < np) {
+            // N+(a_i) holds only vertices after a_i: a hit is past i
+            const int jj = W == 1 ? find32(w) : i + 1 + bsearch_i32(plist + i + 1, np - i - 1, w);
+            if (jj > i) {
+              atomicOr(&rowsT[(jj >> 5) * CAPP + i], 1u << (jj & 31));
+              atomicOr(&rowsT[(i >> 5) * CAPP + jj], 1u << (i & 31));
+            }
+          } else {
+            const int t = i - np;
             const int j = W == 1 ? find32(w) : bsearch_i32(plist, np, w);
             if (j >= 0) atomicOr(&xrowsT[(size_t)(j >> 5) * a.xcap + t], 1u << (j & 31));
-          });
-    }
+          }
+        });
     __syncwarp();
     return nr;
   }

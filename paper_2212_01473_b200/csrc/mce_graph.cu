@@ -783,37 +783,12 @@ k_exact_order(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
 
 // ---- reorder
 
-__global__ void k_reorder_keys(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                               int64_t n, const int64_t* __restrict__ pos, int b,
-                               uint64_t* __restrict__ keys) {
-  const int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    uint64_t pv = (uint64_t)pos[v] << b;
-    for (int64_t e = ro[v] + lane; e < ro[v + 1]; e += 32) keys[e] = pv | (uint64_t)pos[col[e]];
-  }
-}
-
 // ndeg[pos[v]] = deg(v); ndeg[n] = 0 (so an exclusive scan gives n + 1 offsets)
 __global__ void k_permuted_degrees(const int64_t* __restrict__ ro, const int64_t* __restrict__ pos,
                                    int64_t n, int64_t* __restrict__ ndeg) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
        v += (int64_t)gridDim.x * blockDim.x)
     ndeg[v < n ? pos[v] : n] = v < n ? ro[v + 1] - ro[v] : 0;
-}
-
-// one warp per source row: the row's neighbours, relabelled, into row pos[v]
-__global__ void k_scatter_rows(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                               int64_t n, const int64_t* __restrict__ pos,
-                               const int64_t* __restrict__ nro, int32_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    const int64_t src = ro[v], len = ro[v + 1] - src, dst = nro[pos[v]];
-    for (int64_t j = lane; j < len; j += 32) out[dst + j] = (int32_t)pos[col[src + j]];
-  }
 }
 
 // Relabel and sort each row in one pass, one warp per source row: rows of

@@ -25,6 +25,15 @@
 // word w of row c, with column stride CAP+1 so both access patterns are
 // bank-conflict free: lane-per-candidate pivot scans read consecutive
 // columns, lane-per-word row loads read one column across words.
+//
+// Beyond the reference's scheme (results unchanged):
+//  * heavy-X roots (|X| >= HEAVY_X_MIN) take their X rows from a grid-wide
+//    pre-pass (k_heavy_xrows); X members with no neighbour in P start outside
+//    the X_X token list;
+//  * a donated branch borrows its root's induced rows from the owner (every
+//    donation happens after the last root was claimed, so they stay valid);
+//  * the induced-row build walks the P then X members' N+ lists as one
+//    flattened (member, neighbour) stream over the lanes.
 #include <cub/cub.cuh>
 
 #include <algorithm>

@@ -66,9 +66,11 @@ void mce_prepare_device();
 // cudaFreeAsync of its own once the arena has grown to the call's demand
 // (host-side driver calls dominate a millisecond-scale job otherwise).  A call
 // that outgrows it takes the overflow from the stream-ordered pool and the
-// arena is re-sized for the next call.  Held by one call at a time; a
-// concurrent call (another thread) falls back to the pool.  The destructor
-// synchronises the stream unless the call already did (mark_synced()).
+// arena is re-sized (stream-ordered) for the next call.  Reuse is
+// stream-ordered too: releasing records an event and never waits on the host,
+// and a call on another stream waits for that event on the device.  Held by
+// one call at a time on the host; a concurrent call (another thread) falls
+// back to the pool.
 class Scratch {
  public:
   explicit Scratch(cudaStream_t s);
@@ -96,6 +98,9 @@ class Scratch {
 // is a driver round trip that occasionally stalls for milliseconds, too much
 // to pay on every call of a millisecond-scale job.
 size_t mce_free_memory();
+
+// MCE_TRACE=1: host timestamp marks on stderr (diagnostics; no-op otherwise)
+void mce_trace_mark(const char* what);
 
 // count of this library's own kernel launches (mce_launch_count)
 void mce_count_launch(int64_t k = 1);

@@ -56,13 +56,23 @@ struct ArenaState {
   bool busy = false;
   char* base = nullptr;
   size_t cap = 0, want = 0;
+  cudaEvent_t last = nullptr;   // recorded at the end of the last call's work
+  cudaStream_t last_stream = nullptr;
+  bool used = false;
 };
 ArenaState g_arena[64];
 constexpr size_t ARENA_ALIGN = 256;
+bool g_free_stale[64];  // set when the scratch arena re-sizes itself
 }  // namespace
 
-namespace {
-bool g_free_stale[64];  // set when the scratch arena re-sizes itself
+void mce_trace_mark(const char* what) {
+  static const bool on = getenv("MCE_TRACE") != nullptr;
+  if (!on) return;
+  static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[mce_trace] %-22s +%8.3f ms\n", what,
+          std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 size_t mce_free_memory() {
@@ -92,11 +102,19 @@ Scratch::Scratch(cudaStream_t s) : s_(s) {
   if (a.busy) return;
   a.busy = true;
   owner_ = true;
-  if (a.want > a.cap) {  // grow (the previous call left the arena idle: it synchronised)
-    if (a.base) cudaFree(a.base);
+  if (!a.last && cudaEventCreateWithFlags(&a.last, cudaEventDisableTiming) != cudaSuccess) {
+    a.busy = false;
+    owner_ = false;
+    return;
+  }
+  // stream order: this call's work starts after the previous call's work on
+  // the arena (same stream: already ordered; another stream: wait on the device)
+  if (a.used && a.last_stream != s) cudaStreamWaitEvent(s, a.last, 0);
+  if (a.want > a.cap) {  // grow, stream-ordered (no host wait)
+    if (a.base) cudaFreeAsync(a.base, s);
     a.base = nullptr;
     a.cap = 0;
-    if (cudaMalloc((void**)&a.base, a.want) == cudaSuccess) a.cap = a.want;
+    if (cudaMallocAsync((void**)&a.base, a.want, s) == cudaSuccess) a.cap = a.want;
     else a.base = nullptr;
     g_free_stale[dev_] = true;
   }
@@ -121,11 +139,13 @@ int Scratch::raw(void** p, size_t bytes) {
 }
 
 Scratch::~Scratch() {
-  if (!synced_) cudaStreamSynchronize(s_);
   for (void* q : extra_) cudaFreeAsync(q, s_);
   if (owner_) {
     ArenaState& a = g_arena[dev_];
     std::lock_guard<std::mutex> lk(a.mu);
+    cudaEventRecord(a.last, s_);
+    a.last_stream = s_;
+    a.used = true;
     if (demand_ > a.cap) a.want = demand_ + demand_ / 8;
     a.busy = false;
   }
@@ -575,6 +595,7 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
     alive_a[v] = (int32_t)v;
     removed[v] = 0;
   }
+  if (gtid == 0) sh->mindeg = 0x7fffffff;  // the rest of *sh is zeroed by the host
   agrid_barrier(sh, G, nothing);
   int32_t* alive = alive_a;
   int32_t* alive2 = alive_b;
@@ -857,6 +878,45 @@ k_reorder_rows(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, 
   }
 }
 
+// The rows k_reorder_rows listed as long (REORDER_SMEM < len <= LONGROW_MAX):
+// one CTA per row at a time, bitonic sort in shared memory, written in place
+// of the unsorted copy.  (Longer rows -- only the largest R-MAT hubs -- go
+// through a segmented sort instead.)
+constexpr int LONGROW_THREADS = 1024;
+constexpr int LONGROW_MAX = 16384;
+__global__ void __launch_bounds__(LONGROW_THREADS)
+k_sort_long_rows(const int32_t* __restrict__ tmp, int32_t* __restrict__ out,
+                 const int64_t* __restrict__ seg_b, const int64_t* __restrict__ seg_e,
+                 const unsigned long long* __restrict__ nlong) {
+  extern __shared__ int32_t sb[];
+  const unsigned long long cnt = *nlong;
+  for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
+    const int64_t b = seg_b[r];
+    const int len = (int)(seg_e[r] - b);
+    int p2 = 2048;
+    while (p2 < len) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) sb[i] = i < len ? tmp[b + i] : 0x7fffffff;
+    __syncthreads();
+    for (int k = 2; k <= p2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+          const int ij = i ^ j;
+          if (ij > i) {
+            const int32_t x = sb[i], y = sb[ij];
+            if ((x > y) == ((i & k) == 0)) {
+              sb[i] = y;
+              sb[ij] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) out[b + i] = sb[i];
+    __syncthreads();
+  }
+}
+
 __global__ void k_relabel(const int64_t* __restrict__ pos, int64_t n,
                           const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -975,7 +1035,8 @@ unsigned apeel_env(const char* name, unsigned dflt) {  // diagnostics knobs
 }
 
 // Asynchronous peel (method 2); positions to d_pos straight from the claim order.
-int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaStream_t s) {
+int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaStream_t s,
+               Scratch& scr) {
   const int64_t n = g->n;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -996,16 +1057,12 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
   uint8_t* removed = nullptr;
   APeelShared* sh = nullptr;
   const int64_t task_cap = n + g->nnz / 32 + 2 * APEEL_BATCH * grid * (APEEL_THREADS / 32) + 64;
-  if (dev_alloc(&deg, n, s) || dev_alloc(&alive, n, s) || dev_alloc(&alive2, n, s) ||
-      dev_alloc(&order, n, s) || dev_alloc(&tasks, task_cap, s) || dev_alloc(&removed, n, s) ||
-      dev_alloc(&sh, 1, s))
+  if (scr.get(&deg, n) || scr.get(&alive, n) || scr.get(&alive2, n) || scr.get(&order, n) ||
+      scr.get(&tasks, task_cap) || scr.get(&removed, n) || scr.get(&sh, 1))
     return -1;
   MCE_CHECK(cudaMemsetAsync(tasks, 0xff, sizeof(uint64_t) * task_cap, s));
-  MCE_CHECK(cudaMemsetAsync(sh, 0, sizeof(APeelShared), s));
-  {
-    const int big = 0x7fffffff;
-    MCE_CHECK(cudaMemcpyAsync(&sh->mindeg, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-  }
+  MCE_CHECK(cudaMemsetAsync(sh, 0, sizeof(APeelShared), s));  // mindeg: set by the kernel
+  mce_trace_mark("peel setup");
   k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                    removed, order, sh, d_degeneracy,
                                                    apeel_env("MCE_APEEL_POLL", 7),
@@ -1015,26 +1072,24 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
   k_peel_positions<<<grid_for(n), 256, 0, s>>>(order, n, d_pos);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
-  dev_free(deg, s); dev_free(alive, s); dev_free(alive2, s); dev_free(order, s);
-  dev_free(tasks, s); dev_free(removed, s); dev_free(sh, s);
   return 0;
 }
 
 // Degeneracy order into device buffers (positions, degeneracy); no host sync.
-int order_device(const mce_graph* g, int method, int64_t* d_pos, int64_t* d_deg, cudaStream_t s) {
+int order_device(const mce_graph* g, int method, int64_t* d_pos, int64_t* d_deg, cudaStream_t s,
+                 Scratch& scr) {
   const int64_t n = g->n;
   if (method == 1) {
     int64_t leaves = 2;
     while (leaves < n) leaves <<= 1;
     uint64_t* tree = nullptr;
-    if (dev_alloc(&tree, 2 * leaves, s)) return -1;
+    if (scr.get(&tree, 2 * leaves)) return -1;
     k_exact_order<<<1, EXACT_THREADS, 0, s>>>(g->ro, g->col, n, leaves, tree, d_pos, d_deg);
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
-    dev_free(tree, s);
     return 0;
   }
-  if (method == 2) return peel_async(g, d_pos, d_deg, s);
+  if (method == 2) return peel_async(g, d_pos, d_deg, s, scr);
   return peel_parallel(g, d_pos, d_deg, s);
 }
 
@@ -1292,37 +1347,31 @@ int mce_degeneracy_order(const mce_graph* g, int method, int64_t* position,
   const int64_t n = g->n;
   *degeneracy = 0;
   if (n == 0) return 0;
+  Scratch scr(s);
   int64_t* d_pos = position_on_device ? position : nullptr;
   int64_t* d_deg = nullptr;
-  if ((!d_pos && dev_alloc(&d_pos, n, s)) || dev_alloc(&d_deg, 1, s)) return -1;
-  int rc = order_device(g, method, d_pos, d_deg, s);
+  if ((!d_pos && scr.get(&d_pos, n)) || scr.get(&d_deg, 1)) return -1;
+  int rc = order_device(g, method, d_pos, d_deg, s, scr);
   if (rc) return rc;
   MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   if (!position_on_device)
     MCE_CHECK(cudaMemcpyAsync(position, d_pos, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
   MCE_CHECK(cudaStreamSynchronize(s));
-  if (!position_on_device) dev_free(d_pos, s);
-  dev_free(d_deg, s);
   return 0;
 }
 
-int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_device,
-                void* stream, mce_graph** out) {
-  mce_prepare_device();
-  cudaStream_t s = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+// Relabel by device positions into a new graph; temporaries from `scr`.
+int reorder_impl(const mce_graph* g, const int64_t* d_pos, cudaStream_t s, Scratch& scr,
+                 mce_graph** out) {
   *out = nullptr;
   mce_graph* h = new mce_graph();
   h->device = g->device;
   h->n = g->n;
   const int64_t n = g->n;
   const int b = bits_for(std::max<int64_t>(n, 2));
-  const int64_t* d_pos = position;
-  int64_t* owned = nullptr;
-  if (!position_on_device && n > 0) {
-    if (dev_alloc(&owned, n, s)) return -1;
-    MCE_CHECK(cudaMemcpyAsync(owned, position, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
-    d_pos = owned;
-  }
   // Row-wise relabel: the new row pos[v] is v's adjacency mapped through
   // pos, so the new offsets are a scan of the permuted degrees, the rows are
   // scattered whole (coalesced), and only each row needs sorting -- a
@@ -1332,53 +1381,86 @@ int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_dev
   h->nnz = nnz;
   int64_t* ndeg = nullptr;
   int32_t* tmpcol = nullptr;
-  if (dev_alloc(&h->ro, n + 1, s) || dev_alloc(&h->col, nnz, s) || dev_alloc(&ndeg, n + 1, s) ||
-      dev_alloc(&tmpcol, nnz, s) || dev_alloc(&h->labels, n, s))
+  if (dev_alloc(&h->ro, n + 1, s) || dev_alloc(&h->col, nnz, s) || scr.get(&ndeg, n + 1) ||
+      scr.get(&tmpcol, nnz) || dev_alloc(&h->labels, n, s)) {
+    delete h;
     return -1;
+  }
   if (n > 0) {
+    mce_trace_mark("reorder allocs");
     k_permuted_degrees<<<grid_for(n + 1), 256, 0, s>>>(g->ro, d_pos, n, ndeg);
     mce_count_launch();
     size_t tb = 0;
     MCE_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ndeg, h->ro, n + 1, s));
     void* tmp = nullptr;
-    MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+    if (scr.raw(&tmp, tb)) return -1;
     MCE_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, ndeg, h->ro, n + 1, s));
-    cudaFreeAsync(tmp, s);
     if (nnz > 0) {
       // rows sorted in place by k_reorder_rows; the few long ones listed as
       // segments (the rest of the list stays empty) for one segmented sort
       int64_t* seg = nullptr;
-      unsigned long long* nlong = nullptr;
-      if (dev_alloc(&seg, 2 * n, s) || dev_alloc(&nlong, 1, s)) return -1;
-      MCE_CHECK(cudaMemsetAsync(seg, 0, sizeof(int64_t) * 2 * n, s));
-      MCE_CHECK(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), s));
+      if (scr.get(&seg, 2 * n + 1)) return -1;
+      unsigned long long* nlong = reinterpret_cast<unsigned long long*>(seg + 2 * n);
+      MCE_CHECK(cudaMemsetAsync(seg, 0, sizeof(int64_t) * (2 * n + 1), s));
       k_reorder_rows<<<grid_for(n * 32, REORDER_THREADS), REORDER_THREADS, 0, s>>>(
           g->ro, g->col, n, d_pos, h->ro, h->col, tmpcol, seg, seg + n, nlong);
       mce_count_launch();
       MCE_CHECK(cudaGetLastError());
-      tb = 0;
-      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmpcol, h->col, nnz, n, seg,
-                                                   seg + n, s));
-      MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
-      MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, tmpcol, h->col, nnz, n, seg,
-                                                   seg + n, s));
-      cudaFreeAsync(tmp, s);
-      dev_free(seg, s);
-      dev_free(nlong, s);
+      // rows up to LONGROW_MAX: one CTA each (no host round trip); the
+      // segmented sort (which reads its partition sizes back to the host)
+      // only when the graph has longer rows
+      if (mce_graph_sync_stats(g)) return -1;
+      if (g->max_degree <= LONGROW_MAX) {
+        static bool attr = false;
+        if (!attr) {
+          MCE_CHECK(cudaFuncSetAttribute(k_sort_long_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(LONGROW_MAX * sizeof(int32_t))));
+          attr = true;
+        }
+        k_sort_long_rows<<<296, LONGROW_THREADS, LONGROW_MAX * sizeof(int32_t), s>>>(
+            tmpcol, h->col, seg, seg + n, nlong);
+        mce_count_launch();
+        MCE_CHECK(cudaGetLastError());
+      } else {
+        tb = 0;
+        MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmpcol, h->col, nnz, n, seg,
+                                                     seg + n, s));
+        if (scr.raw(&tmp, tb)) return -1;
+        MCE_CHECK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, tmpcol, h->col, nnz, n, seg,
+                                                     seg + n, s));
+      }
     }
+    mce_trace_mark("reorder sorts queued");
     k_relabel<<<grid_for(n), 256, 0, s>>>(d_pos, n, g->labels, h->labels);
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
   } else {
     MCE_CHECK(cudaMemsetAsync(h->ro, 0, sizeof(int64_t), s));
   }
-  dev_free(ndeg, s);
-  dev_free(tmpcol, s);
-  dev_free(owned, s);
   int rc = mce_graph_build_split(h, s);
+  mce_trace_mark("split queued");
   if (rc) { mce_graph_free(h); return rc; }
   *out = h;
   return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int mce_reorder(const mce_graph* g, const int64_t* position, int position_on_device,
+                void* stream, mce_graph** out) {
+  mce_prepare_device();
+  cudaStream_t s = (cudaStream_t)stream;
+  *out = nullptr;
+  Scratch scr(s);
+  const int64_t* d_pos = position;
+  if (!position_on_device && g->n > 0) {
+    int64_t* owned = nullptr;
+    if (scr.get(&owned, g->n)) return -1;
+    MCE_CHECK(cudaMemcpyAsync(owned, position, sizeof(int64_t) * g->n, cudaMemcpyHostToDevice, s));
+    d_pos = owned;
+  }
+  return reorder_impl(g, d_pos, s, scr, out);
 }
 
 // Order + relabel without leaving the device (graph.py:239-243 minus stats):
@@ -1390,16 +1472,22 @@ int mce_preprocess(const mce_graph* g, int method, int64_t* degeneracy, void* st
   *out = nullptr;
   if (degeneracy) *degeneracy = 0;
   if (g->n == 0) return mce_reorder(g, nullptr, 1, stream, out);
+  mce_trace_mark("preprocess enter");
+  Scratch scr(s);  // every temporary of order + reorder, released stream-ordered
+  mce_trace_mark("pp scratch");
   int64_t* d_pos = nullptr;
   int64_t* d_deg = nullptr;
-  if (dev_alloc(&d_pos, g->n, s) || dev_alloc(&d_deg, 1, s)) return -1;
-  int rc = order_device(g, method, d_pos, d_deg, s);
-  if (!rc) rc = mce_reorder(g, d_pos, 1, stream, out);  // ends with a stream sync
+  if (scr.get(&d_pos, g->n) || scr.get(&d_deg, 1)) return -1;
+  int rc = order_device(g, method, d_pos, d_deg, s, scr);
+  mce_trace_mark("pp order queued");
+  if (!rc) rc = reorder_impl(g, d_pos, s, scr, out);
+  mce_trace_mark("pp reorder queued");
   // NULL degeneracy: no wait (the reordered graph's max |N+(v)| is the degeneracy,
   // available through mce_graph_info)
-  if (!rc && degeneracy) MCE_CHECK(cudaMemcpy(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost));
-  dev_free(d_pos, s);
-  dev_free(d_deg, s);
+  if (!rc && degeneracy) {
+    MCE_CHECK(cudaMemcpyAsync(degeneracy, d_deg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    MCE_CHECK(cudaStreamSynchronize(s));
+  }
   return rc;
 }
 

@@ -292,25 +292,27 @@ def main():
 
     # algorithmic bytes of one step's induced-subgraph builds (outside the timing)
     build_bytes_step = one_job(g, measure=True)[0].build_bytes
-    # W warm-up steps, and at least ~0.5 s of them: a fresh box starts at idle
-    # clocks and an empty stream-ordered memory pool
-    t_w = time.perf_counter()
-    w_done = 0
-    while w_done < max(args.warmup, 3) or (time.perf_counter() - t_w < 0.5 and w_done < 1000):
-        res, tot, st = one_job(g)
-        w_done += 1
-    torch.cuda.synchronize()
-    # ---- device-resident timed region ------------------------------------
-    kernel_ms = 0.0
-    launches0 = _lib.lib().mce_launch_count()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # 2x the 126 MB L2
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     import gc
 
-    gc.collect()
-    gc.disable()  # no collector pauses between the kernels of a timed step
     with ClockSampler(local, enabled=not args.no_clocks) as clocks:
+        # W warm-up steps shaped like the timed ones (L2 flush first), and at
+        # least ~0.5 s of them: a fresh box starts at idle clocks and an empty
+        # stream-ordered memory pool
+        t_w = time.perf_counter()
+        w_done = 0
+        while w_done < max(args.warmup, 3) or (time.perf_counter() - t_w < 0.5 and w_done < 1000):
+            flush.zero_()
+            res, tot, st = one_job(g)
+            w_done += 1
+        torch.cuda.synchronize()
+        # ---- device-resident timed region ----------------------------------
+        kernel_ms = 0.0
+        launches0 = _lib.lib().mce_launch_count()
+        gc.collect()
+        gc.disable()  # no collector pauses between the kernels of a timed step
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()

@@ -41,6 +41,7 @@
 #include <mutex>
 #include <cstdlib>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "mce_common.cuh"
@@ -1764,6 +1765,20 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   }
   cudaEvent_t* events = ev_cache[ev_dev];
   int nev = 0;
+  // pinned staging for the D2H reads of this call (guarded by ev_lock): the
+  // zeroed block comes back in ONE copy; pageable destinations would be
+  // staged by the driver and cost tens of microseconds each
+  static unsigned long long* pin_buf[64];
+  static size_t pin_cap[64];
+  if (pin_cap[ev_dev] < zwords) {
+    if (pin_buf[ev_dev]) cudaFreeHost(pin_buf[ev_dev]);
+    pin_buf[ev_dev] = nullptr;
+    pin_cap[ev_dev] = 0;
+    MCE_CHECK(cudaHostAlloc((void**)&pin_buf[ev_dev], zwords * sizeof(unsigned long long),
+                            cudaHostAllocPortable));
+    pin_cap[ev_dev] = zwords;
+  }
+  unsigned long long* pin = pin_buf[ev_dev];
   tr.mark("vhash+events");
   if (count > 0) {
     uint32_t *keys = nullptr, *keys2 = nullptr;
@@ -1805,8 +1820,9 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     void* tmp = nullptr;
     if (scr.raw(&tmp, tb)) return -1;
     MCE_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, count, 0, 24, s));
-    unsigned long long hc[HMETA + 3];
-    MCE_CHECK(cudaMemcpyAsync(hc, cls, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    unsigned long long* hc = pin + ZB_CLS;  // pinned: cls[0 .. HMETA + 3)
+    MCE_CHECK(cudaMemcpyAsync(hc, cls, (HMETA + 3) * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s));
     tr.mark("root keys+sort queued");
     MCE_CHECK(cudaStreamSynchronize(s));
     tr.mark("class counts synced");
@@ -1959,28 +1975,30 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
   }
-  unsigned long long h_acc[8];
-  unsigned long long h_len = 0, h_bytes = 0;
-  MCE_CHECK(cudaMemcpyAsync(&h_bytes, bb, sizeof(h_bytes), cudaMemcpyDeviceToHost, s));
-  MCE_CHECK(cudaMemcpyAsync(h_acc, acc, sizeof(h_acc), cudaMemcpyDeviceToHost, s));
-  MCE_CHECK(cudaMemcpyAsync(out->hist, hist, sizeof(int64_t) * HIST_MAX, cudaMemcpyDeviceToHost, s));
-  MCE_CHECK(cudaMemcpyAsync(&h_len, collect_len, sizeof(h_len), cudaMemcpyDeviceToHost, s));
+  // one D2H of the zeroed block (counters, histogram, stream length, worker
+  // metrics of the slots in use), then host copies out of the pinned staging
+  const int64_t wslots = (worker_metrics && worker_metrics_cap > 0)
+                             ? std::min<int64_t>(worker_metrics_cap, max_workers_slots)
+                             : 0;
+  const size_t back = (size_t)ZB_CLS + 16 + 4 * (size_t)std::max<int64_t>(wslots, 0);
+  MCE_CHECK(cudaMemcpyAsync(pin, zb, back * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   tr.mark("results queued");
   MCE_CHECK(cudaStreamSynchronize(s));
   tr.mark("results synced");
+  unsigned long long h_acc[8];
+  memcpy(h_acc, pin, sizeof(h_acc));
+  memcpy(out->hist, pin + 8, sizeof(int64_t) * HIST_MAX);
+  const unsigned long long h_len = pin[8 + HIST_MAX];
+  const unsigned long long h_bytes = pin[8 + HIST_MAX + 1];
+  if (wslots > 0) memcpy(worker_metrics, pin + ZB_CLS + 16, sizeof(int64_t) * 4 * wslots);
   if (collect && cfg->collect_cap > 0) {
     int64_t words = std::min<int64_t>((int64_t)h_len, cfg->collect_cap);
-    if (words > 0)
+    if (words > 0) {
       MCE_CHECK(cudaMemcpyAsync(collect, d_collect, sizeof(int64_t) * words,
                                 cudaMemcpyDeviceToHost, s));
+      MCE_CHECK(cudaStreamSynchronize(s));
+    }
   }
-  if (worker_metrics && wmet && worker_metrics_cap > 0) {
-    int64_t slots = std::min<int64_t>(worker_metrics_cap, max_workers_slots);
-    if (slots > 0)
-      MCE_CHECK(cudaMemcpyAsync(worker_metrics, wmet, sizeof(int64_t) * 4 * slots,
-                                cudaMemcpyDeviceToHost, s));
-  }
-  MCE_CHECK(cudaStreamSynchronize(s));
   scr.mark_synced();
   out->cliques = (int64_t)h_acc[0];
   out->hash = (uint64_t)h_acc[1];

@@ -812,62 +812,83 @@ __global__ void k_permuted_degrees(const int64_t* __restrict__ ro, const int64_t
     ndeg[v < n ? pos[v] : n] = v < n ? ro[v + 1] - ro[v] : 0;
 }
 
-// Relabel and sort each row in one pass, one warp per source row: rows of
-// <= 32 entries are sorted in registers (bitonic network over the lanes),
-// rows of <= REORDER_SMEM entries by a bitonic sort in the warp's shared
-// memory; longer rows are written unsorted to `tmp` and listed as segments
-// (begin/end) for one segmented sort afterwards.
+// Bitonic sort of 32*E values held E per lane (element lane*E + e),
+// ascending: exchanges between lanes by shuffles, within a lane in registers.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(int32_t (&x)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int idx = lane * E + e;
+          const int32_t y = __shfl_xor_sync(0xffffffffu, x[e], lj);
+          const bool up = (idx & k) == 0, lower = (lane & lj) == 0;
+          x[e] = (lower == up) ? min(x[e], y) : max(x[e], y);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int q = e ^ j;
+          if (q > e) {
+            const bool up = ((lane * E + e) & k) == 0;
+            const int32_t a = x[e], b = x[q];
+            const bool sw = (a > b) == up;
+            x[e] = sw ? b : a;
+            x[q] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+// one row of d <= 32*E entries: map through pos, sort, store
+template <int E>
+__device__ __forceinline__ void reorder_row(const int32_t* __restrict__ col,
+                                            const int64_t* __restrict__ pos, int64_t src, int d,
+                                            int32_t* __restrict__ out, int64_t dst, int lane) {
+  int32_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int idx = lane * E + e;
+    x[e] = idx < d ? (int32_t)pos[col[src + idx]] : 0x7fffffff;
+  }
+  warp_bitonic<E>(x, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int idx = lane * E + e;
+    if (idx < d) out[dst + idx] = x[e];
+  }
+}
+
+// Relabel and sort each row in one pass, one warp per source row: rows of up
+// to REORDER_REG entries are sorted in registers (a warp bitonic network over
+// E = ceil(d/32) <= 8 values per lane); longer rows are written unsorted to
+// `tmp` and listed as segments (begin/end) for k_sort_long_rows.
 constexpr int REORDER_THREADS = 256;
-constexpr int REORDER_SMEM = 1024;
+constexpr int REORDER_REG = 256;
 __global__ void __launch_bounds__(REORDER_THREADS)
 k_reorder_rows(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                const int64_t* __restrict__ pos, const int64_t* __restrict__ nro,
                int32_t* __restrict__ out, int32_t* __restrict__ tmp, int64_t* __restrict__ seg_b,
                int64_t* __restrict__ seg_e, unsigned long long* __restrict__ nlong) {
-  __shared__ int32_t sbuf[REORDER_THREADS / 32][REORDER_SMEM];
   const int lane = threadIdx.x & 31;
-  int32_t* buf = sbuf[threadIdx.x >> 5];
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t v = warp; v < n; v += nwarps) {
     const int64_t src = ro[v];
     const int d = (int)(ro[v + 1] - src);
     const int64_t dst = nro[pos[v]];
-    if (d <= 32) {
-      int32_t x = lane < d ? (int32_t)pos[col[src + lane]] : 0x7fffffff;
-#pragma unroll
-      for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-          const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-          x = (lower == up) ? min(x, y) : max(x, y);
-        }
-      }
-      if (lane < d) out[dst + lane] = x;
-    } else if (d <= REORDER_SMEM) {
-      int p2 = 64;
-      while (p2 < d) p2 <<= 1;
-      for (int i = lane; i < p2; i += 32) buf[i] = i < d ? (int32_t)pos[col[src + i]] : 0x7fffffff;
-      __syncwarp();
-      for (int k = 2; k <= p2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = lane; i < p2; i += 32) {
-            const int ij = i ^ j;
-            if (ij > i) {
-              const int32_t a = buf[i], b = buf[ij];
-              if ((a > b) == ((i & k) == 0)) {
-                buf[i] = b;
-                buf[ij] = a;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-      for (int i = lane; i < d; i += 32) out[dst + i] = buf[i];
-      __syncwarp();
-    } else {
+    if (d <= 32) reorder_row<1>(col, pos, src, d, out, dst, lane);
+    else if (d <= 64) reorder_row<2>(col, pos, src, d, out, dst, lane);
+    else if (d <= 128) reorder_row<4>(col, pos, src, d, out, dst, lane);
+    else if (d <= REORDER_REG) reorder_row<8>(col, pos, src, d, out, dst, lane);
+    else {
       for (int i = lane; i < d; i += 32) tmp[dst + i] = (int32_t)pos[col[src + i]];
       if (lane == 0) {
         const unsigned long long idx = atomicAdd(nlong, 1ull);
@@ -878,7 +899,7 @@ k_reorder_rows(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, 
   }
 }
 
-// The rows k_reorder_rows listed as long (REORDER_SMEM < len <= LONGROW_MAX):
+// The rows k_reorder_rows listed as long (REORDER_REG < len <= LONGROW_MAX):
 // one CTA per row at a time, bitonic sort in shared memory, written in place
 // of the unsorted copy.  (Longer rows -- only the largest R-MAT hubs -- go
 // through a segmented sort instead.)
@@ -893,7 +914,7 @@ k_sort_long_rows(const int32_t* __restrict__ tmp, int32_t* __restrict__ out,
   for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
     const int64_t b = seg_b[r];
     const int len = (int)(seg_e[r] - b);
-    int p2 = 2048;
+    int p2 = 256;
     while (p2 < len) p2 <<= 1;
     for (int i = threadIdx.x; i < p2; i += blockDim.x) sb[i] = i < len ? tmp[b + i] : 0x7fffffff;
     __syncthreads();

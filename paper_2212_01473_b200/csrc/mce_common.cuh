@@ -84,12 +84,11 @@ class Scratch {
   }
   int raw(void** p, size_t bytes);
   size_t reserved() const;  // arena bytes this call may use (already held, not in free memory)
-  void mark_synced() { synced_ = true; }
 
  private:
   cudaStream_t s_;
   int dev_ = 0;
-  bool owner_ = false, synced_ = false;
+  bool owner_ = false;
   size_t used_ = 0, demand_ = 0;
   std::vector<void*> extra_;
 };

@@ -1999,7 +1999,6 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       MCE_CHECK(cudaStreamSynchronize(s));
     }
   }
-  scr.mark_synced();
   out->cliques = (int64_t)h_acc[0];
   out->hash = (uint64_t)h_acc[1];
   out->nodes = (int64_t)h_acc[2] + trivial_nodes;

@@ -5,11 +5,14 @@ histogram and clique-set hash."""
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import pytest
 
 from conftest import K4_TRIANGLE_CLIQUES, K4_TRIANGLE_EDGES, golden_cases
 from oracle import oracle
+from paper_2212_01473_b200 import generate
 from paper_2212_01473_b200 import (
     CliqueSink,
     RunConfig,
@@ -205,3 +208,20 @@ def test_l2_roots_count_isolated_vertices():
     g2, _, st = preprocess(g)
     res = run(g2, st, RunConfig(workers=2, roots="l2", induced="ipx"))
     assert res.clique_count == 3
+
+
+def test_scratch_arena_is_stream_ordered():
+    """Temporaries come from a per-device arena released without a host wait;
+    a call on another stream must wait for the previous call's work on the
+    device (cudaStreamWaitEvent): alternating streams give identical results."""
+    import torch
+
+    edges, n = generate.workload_edges("er2k")
+    g2, _, st = preprocess(from_edges(edges, n))
+    base = run(g2, st, RunConfig())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for i in range(6):
+        s = streams[i % 2]
+        res = run(g2, st, RunConfig(), stream=ctypes.c_void_p(s.cuda_stream))
+        assert (res.clique_count, res.clique_hash, res.nodes_total) == \
+            (base.clique_count, base.clique_hash, base.nodes_total)

@@ -59,7 +59,10 @@ constexpr int XROWS_PARTIAL_MAX = 2048;  // partial mode: X rows for roots with 
 // pre-pass (k_heavy_xrows) instead of one warp's walk over sum |N+(x)|: a hub
 // late in the order would otherwise bound the whole launch.  Their pool slot
 // (+1) rides in the root word above ROOT_ID_BITS.
-constexpr int HEAVY_X_MIN = 256;
+#ifndef MCE_HEAVY_X_MIN
+#define MCE_HEAVY_X_MIN 256
+#endif
+constexpr int HEAVY_X_MIN = MCE_HEAVY_X_MIN;
 constexpr int HEAVY_MAX = 16384;        // heavy slots
 constexpr int HEAVY_UNIT_X = 256;       // X members per pre-pass CTA
 constexpr int HEAVY_UNITS_MAX = 1 << 20;

@@ -1086,8 +1086,8 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
   mce_trace_mark("peel setup");
   k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                    removed, order, sh, d_degeneracy,
-                                                   apeel_env("MCE_APEEL_POLL", 7),
-                                                   apeel_env("MCE_APEEL_SLEEP", 64));
+                                                   apeel_env("MCE_APEEL_POLL", 3),
+                                                   apeel_env("MCE_APEEL_SLEEP", 32));
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   k_peel_positions<<<grid_for(n), 256, 0, s>>>(order, n, d_pos);

@@ -16,9 +16,12 @@ maximal clique counting time").
 * ``cpu_baseline`` -- the reference algorithm (C restatement in oracle/, all
                 host threads) on a bounded sample of the same workload.
 
-Default workload: configs[1] (Barabasi-Albert n=200k, m=8).  N>1 shards the
-first-level subtrees across ranks (no data-path collective; one NCCL
-all-reduce of counts and clique-set hashes); scaling is "strong".
+Default workload: configs[3] (planted cliques, ER n=1M avg deg 20 + 1k
+cliques of size 30-60) -- the largest BASELINE config whose full enumeration
+fits a bench step (rmat20's core alone takes minutes: see DESIGN.md).  N>1
+shards the first-level subtrees across ranks (every rank computes the same
+deterministic ordering; no data-path collective; one NCCL all-reduce of
+counts, histogram and clique-set hash); scaling is "strong".
 """
 
 from __future__ import annotations
@@ -44,6 +47,18 @@ WORKLOAD_CONFIG = {
     "rmat24": "RMAT scale-24, edge factor 16",
 }
 FALLBACK_HBM_GBS = 6650.0
+L2_POLICY = ("GPU arm: a 256 MiB buffer is zeroed between timed steps (outside the CUDA "
+             "events), so every step starts from a cold L2; CPU arm: not applicable")
+ORDERING = {"async": "async peel (degeneracy order, no rounds inside a level)",
+            "parallel": "parallel bucket peel (deterministic degeneracy order, same on every rank)",
+            "exact": "the reference's exact degeneracy order"}
+
+
+def workload_config(name, n, m, degeneracy, max_degree, roots, induced) -> dict:
+    """The workload both arms report (identical keys and values)."""
+    return {"workload": WORKLOAD_CONFIG[name], "name": name, "n": int(n), "m": int(m),
+            "degeneracy": int(degeneracy), "max_degree": int(max_degree), "roots": roots,
+            "induced": induced, "l2_flush": L2_POLICY}
 METRIC = "maximal cliques/sec (end-to-end MCE: degeneracy order + reorder + enumerate)"
 
 
@@ -52,7 +67,7 @@ def parse_args():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--workload", default=os.environ.get("MCE_BENCH_WORKLOAD", "ba200k"),
+    p.add_argument("--workload", default=os.environ.get("MCE_BENCH_WORKLOAD", "planted1m"),
                    choices=sorted(WORKLOAD_CONFIG))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--seed", type=int, default=0)
@@ -207,12 +222,12 @@ def cpu_reference_step(ro, ci, root_stride: int, threads: int, pre=None):
     reorder, enumeration of a strided root sample (oracle/, C + numpy)."""
     from oracle import oracle
 
-    ro2, ci2, d = pre if pre is not None else cpu_preprocess(ro, ci)
+    ro2, ci2, d, labels = pre if pre is not None else cpu_preprocess(ro, ci)
     n = len(ro) - 1
     max_degree = int(np.diff(ro2).max()) if n else 0
     induced = "ip" if d > 0 and max_degree / d > 200.0 else "ipx"
     return oracle.enumerate_cliques(ro2, ci2, roots="l1", induced=induced, degeneracy=d,
-                                    root_stride=root_stride, threads=threads)
+                                    labels=labels, root_stride=root_stride, threads=threads)
 
 
 def cpu_preprocess(ro, ci):
@@ -220,7 +235,9 @@ def cpu_preprocess(ro, ci):
 
     pos, d = oracle.degeneracy_order(ro, ci)
     ro2, ci2 = oracle.reorder(ro, ci, pos)
-    return ro2, ci2, d
+    labels = np.empty_like(pos)
+    labels[pos] = np.arange(len(pos), dtype=pos.dtype)  # original id of every rank
+    return ro2, ci2, d, labels
 
 
 def choose_cpu_stride(ro, ci, target_s: float, threads: int) -> tuple[int, float, dict]:
@@ -254,25 +271,29 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2212_01473_b200 import RunConfig, from_device_edges, preprocess
     from paper_2212_01473_b200 import _lib
-    from paper_2212_01473_b200.distributed import run_sharded, run_work_stealing
+    from paper_2212_01473_b200.distributed import (run_sharded, run_work_stealing,
+                                                   shard_order_method)
     from paper_2212_01473_b200.graph import from_edges
 
     _lib.require_device()
     edges, n = load_workload(args.workload, args.seed, on_device=True)
+    # the e2e arm ships the edge list as int32 pairs (ids < 2^31): half the H2D
     if isinstance(edges, np.ndarray):
-        host_edges = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory()
-        dev_edges = host_edges.cuda()
+        dev_edges = torch.from_numpy(np.ascontiguousarray(edges)).cuda()
+        host_edges = torch.from_numpy(np.ascontiguousarray(edges, dtype=np.int32)).pin_memory()
     else:
         dev_edges = edges
-        host_edges = edges.cpu().pin_memory()
+        host_edges = edges.to(torch.int32).cpu().pin_memory()
     torch.cuda.synchronize()
     g = from_device_edges(dev_edges, dev_edges.shape[0], n)
     del dev_edges
     cfg = RunConfig(roots="l1", induced="auto")
     stride = max(1, args.root_stride)
 
+    order_method = shard_order_method(world)  # deterministic whenever ranks share the roots
+
     def one_job(graph, measure=False):
-        g2, _, st = preprocess(graph)
+        g2, _, st = preprocess(graph, method=order_method)
         if world > 1 and stride == 1 and args.shard == "steal":
             results, tot = run_work_stealing(g2, st, cfg, rank, world, device="cuda",
                                              measure_bytes=measure)
@@ -378,16 +399,14 @@ def main():
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_CONFIG[args.workload], "name": args.workload,
-                   "n": n, "m": st.m, "degeneracy": st.degeneracy,
-                   "max_degree": st.max_degree, "roots": cfg.roots,
-                   "induced": res.induced_mode, "root_stride": stride,
-                   "maximal_cliques": count, "nodes": nodes, "clique_hash": chash,
-                   "ordering": "async peel (degeneracy order, no rounds inside a level)", "sharding": args.shard if world > 1 else None,
-                   "l2_flush": "256 MiB buffer zeroed between timed steps, outside the "
-                               "CUDA events"},
+        "config": workload_config(args.workload, n, st.m, st.degeneracy, st.max_degree,
+                                  cfg.roots, res.induced_mode),
+        "result": {"maximal_cliques": count, "nodes": nodes, "clique_hash": chash,
+                   "root_stride": stride,
+                   "ordering": ORDERING[order_method],
+                   "sharding": args.shard if world > 1 else None},
         "e2e": ({"value": count / (e2e_ms / 1e3), "unit": "cliques/s", "ms_per_step": e2e_ms,
-                 "h2d_bytes_per_step": int(host_edges.numel() * 8),
+                 "h2d_bytes_per_step": int(host_edges.numel() * host_edges.element_size()),
                  "d2h_bytes_per_step": int(8 * (10 + 4096))} if e2e_ms else None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
@@ -450,20 +469,29 @@ def run_reference(args, rank: int, world: int):
         stride, _, _ = choose_cpu_stride(ro, ci, 20.0, threads)
     times = []
     out = None
+    pre = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        out = cpu_reference_step(ro, ci, stride, threads)
+        pre = cpu_preprocess(ro, ci)
+        out = cpu_reference_step(ro, ci, stride, threads, pre)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
     val = out["count"] / sec
-    sample = "all first-level roots" if stride == 1 else f"every {stride}-th first-level root"
+    d = pre[2]
+    max_degree = int(np.diff(ro).max()) if n else 0
+    induced = "ip" if d > 0 and max_degree / d > 200.0 else "ipx"
+    sample = ("all first-level roots" if stride == 1 else f"every {stride}-th first-level root") + \
+        "; exact degeneracy order + reorder + enumeration per step"
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "cliques/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": WORKLOAD_CONFIG[args.workload], "name": args.workload,
-                       "maximal_cliques": out["count"], "root_stride": stride},
+            "config": workload_config(args.workload, n, int(len(ci) // 2), d, max_degree, "l1",
+                                      induced),
+            "result": {"maximal_cliques": out["count"], "nodes": out["nodes"],
+                       "clique_hash": out["hash"], "root_stride": stride,
+                       "ordering": ORDERING["exact"], "sharding": None},
             "cpu_baseline": {"value": val, "unit": "cliques/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": val, "unit": "cliques/s", "h2d_bytes_per_step": 0,

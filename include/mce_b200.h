@@ -54,6 +54,13 @@ const char* mce_last_error(void);
 int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
                          int edges_on_device, void* stream, mce_graph** out);
 
+/* The same from 2*num_edges int32 values (ids are below 2^31 anyway): half
+ * the host->device bytes of mce_graph_from_edges for the same graph.  The
+ * reference's from_edges (graph.py:103-129) takes any integer array; this is
+ * the entry a caller holding int32 pairs binds. */
+int mce_graph_from_edges32(const int32_t* edges, int64_t num_edges, int64_t num_vertices,
+                           int edges_on_device, void* stream, mce_graph** out);
+
 /* Edge-list TEXT -> canonical graph, parsed on the device (graph.py:132-180
  * parse_edge_list): '#'/'%' comment lines, "%%MatrixMarket" header (1-based
  * ids after it, the next data line is the size line), two integer tokens per

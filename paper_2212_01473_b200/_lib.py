@@ -67,6 +67,9 @@ EXPORTS = {
     "mce_graph_from_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int, ctypes.c_void_p,
                                             ctypes.POINTER(ctypes.c_void_p)]),
+    "mce_graph_from_edges32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.POINTER(ctypes.c_void_p)]),
     "mce_graph_from_text": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_int, ctypes.c_void_p,
                                            ctypes.POINTER(ctypes.c_void_p),

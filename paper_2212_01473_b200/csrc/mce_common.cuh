@@ -49,8 +49,12 @@ struct mce_graph {
   unsigned long long* stats_dev = nullptr;  // 3 words
   void* stats_slot = nullptr;               // pinned host words + completion event
   bool stats_pending = false;
-  uint64_t* vhash = nullptr;  // mix64(label or id) per vertex, built by the first enumeration
-  int vhash_labels = -1;      // which of the two it holds (-1: not built)
+  // mix64(id) [0] / mix64(label) [1] per vertex: each built once, by the first
+  // enumeration that hashes that way, and never rebuilt -- concurrent calls on
+  // the same graph take the per-graph lock for the build and wait on the
+  // table's event (stream-ordered) before reading it
+  uint64_t* vhash_tab[2] = {nullptr, nullptr};
+  cudaEvent_t vhash_ev[2] = {nullptr, nullptr};
 };
 
 int mce_graph_build_split(mce_graph* g, cudaStream_t s);
@@ -84,6 +88,7 @@ class Scratch {
   }
   int raw(void** p, size_t bytes);
   size_t reserved() const;  // arena bytes this call may use (already held, not in free memory)
+  size_t demand() const { return demand_; }  // bytes this call has taken so far
 
  private:
   cudaStream_t s_;

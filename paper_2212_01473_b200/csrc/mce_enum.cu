@@ -1369,7 +1369,7 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
       roots[i] = (u << 32) | v;
     }
     const int rank = (roots_mode == 1 && p == 0) ? TRIVIAL_RANK : width_rank(p);
-    if (hp.enabled && roots_mode == 1 && p > 0 && x >= HEAVY_X_MIN) {
+    if (hp.enabled && roots_mode == 1 && p > 0 && p <= MAX_CAPACITY_BITS && x >= HEAVY_X_MIN) {
       // reserve a slot, pool words (|X| x W) and pre-pass CTAs for this root
       const unsigned long long slot = atomicAdd(&hp.meta[0], 1ull);
       if (slot < HEAVY_MAX) {
@@ -1377,7 +1377,15 @@ __global__ void k_root_keys(const int64_t* __restrict__ ro, const int64_t* __res
         const unsigned long long off = atomicAdd(&hp.meta[1], words);
         const unsigned long long units = (x + HEAVY_UNIT_X - 1) / HEAVY_UNIT_X;
         if (off + words <= hp.pool_cap) {
-          const unsigned long long u0 = atomicAdd(&hp.meta[2], units);
+          // advance the pre-pass CTA count only when the reservation fits, so
+          // every CTA the host launches (meta[2]) has a written unit_slot
+          unsigned long long u0 = *(volatile unsigned long long*)&hp.meta[2];
+          for (;;) {
+            if (u0 + units > HEAVY_UNITS_MAX) break;
+            const unsigned long long seen = atomicCAS(&hp.meta[2], u0, u0 + units);
+            if (seen == u0) break;
+            u0 = seen;
+          }
           if (u0 + units <= HEAVY_UNITS_MAX) {
             hp.vertex[slot] = r;
             hp.off[slot] = (int64_t)off;
@@ -1713,16 +1721,27 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t stride = cfg->root_stride > 0 ? cfg->root_stride : 1;
   int64_t count = end > begin ? (end - begin + stride - 1) / stride : 0;
 
-  // per-vertex hash terms: built once per graph (and labelling choice)
+  // per-vertex hash terms: built once per graph and labelling choice (never
+  // rebuilt, so a concurrent call on the same graph cannot see a table change
+  // under it); the build is guarded and every reader waits for its event
   mce_graph* gm = const_cast<mce_graph*>(g);
   const int want_labels = (cfg->hash_labels && g->labels) ? 1 : 0;
-  if (gm->vhash_labels != want_labels) {
-    if (!gm->vhash && dalloc(&gm->vhash, n, s)) return -1;
-    k_vhash<<<grid_for(n), 256, 0, s>>>(want_labels ? g->labels : nullptr, n, gm->vhash);
-    mce_count_launch();
-    gm->vhash_labels = want_labels;
+  {
+    static std::mutex vh_mu;
+    std::lock_guard<std::mutex> lk(vh_mu);
+    if (!gm->vhash_tab[want_labels]) {
+      uint64_t* tab = nullptr;
+      if (dalloc(&tab, n, s)) return -1;
+      k_vhash<<<grid_for(n), 256, 0, s>>>(want_labels ? g->labels : nullptr, n, tab);
+      mce_count_launch();
+      MCE_CHECK(cudaEventCreateWithFlags(&gm->vhash_ev[want_labels], cudaEventDisableTiming));
+      MCE_CHECK(cudaEventRecord(gm->vhash_ev[want_labels], s));
+      gm->vhash_tab[want_labels] = tab;
+    } else {
+      MCE_CHECK(cudaStreamWaitEvent(s, gm->vhash_ev[want_labels], 0));
+    }
   }
-  const uint64_t* vhash = g->vhash;
+  const uint64_t* vhash = gm->vhash_tab[want_labels];
   int64_t metric_slots = 0;
   {
     int dev = 0, sms = 0;
@@ -1838,6 +1857,17 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
                               (double)g->max_degree / (double)g->max_later > 200.0);
     out->induced_full = full ? 1 : 0;
     const int64_t* sorted_roots = dv.Current();
+    // capacity first: nothing below may run for a root wider than the widest class
+    // (k_heavy_xrows stages P in a MAX_CAPACITY_BITS shared array)
+    const int64_t cap_limit = std::min<int64_t>(
+        cfg->capacity_bits > 0 ? cfg->capacity_bits : MAX_CAPACITY_BITS, MAX_CAPACITY_BITS);
+    const int64_t max_p = (int64_t)hc[MAXP_SLOT];
+    if (max_p > cap_limit) {
+      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld", (long long)max_p,
+                    (long long)cap_limit);
+      cleanup();
+      return -4;
+    }
     // heavy-X roots: their X rows over the whole grid, before the enumeration
     uint32_t* heavy_pool = nullptr;
     const unsigned long long heavy_units = std::min<unsigned long long>(hc[HMETA + 2], HEAVY_UNITS_MAX);
@@ -1860,15 +1890,6 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       return -1;
     }
     if (prof_cycles) MCE_CHECK(cudaMemsetAsync(prof_cycles, 0, sizeof(long long) * count, s));
-    const int64_t cap_limit = std::min<int64_t>(
-        cfg->capacity_bits > 0 ? cfg->capacity_bits : MAX_CAPACITY_BITS, MAX_CAPACITY_BITS);
-    const int64_t max_p = (int64_t)hc[MAXP_SLOT];
-    if (max_p > cap_limit) {
-      mce_set_error("CapacityError: |P| = %lld exceeds capacity %lld", (long long)max_p,
-                    (long long)cap_limit);
-      cleanup();
-      return -4;
-    }
     const int widths[NUM_WIDTHS] = {128, 64, 32, 16, 8, 4, 2, 1};
     std::vector<ClassPlan> plan;
     int64_t i = 0;
@@ -1880,9 +1901,14 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     const int64_t trivial_count = count - i;
     int64_t wcap = 0;
     double frac = cfg->mem_fraction > 0 ? cfg->mem_fraction : 0.5;
-    size_t budget = (size_t)(avail_b * frac);
+    const size_t budget0 = (size_t)(avail_b * frac);
+    const size_t demand0 = scr.demand();
     // per-worker metrics (zeroed above) accumulate across class launches
     for (const ClassPlan& cp : plan) {
+      // scratch of the earlier classes stays held until the call returns:
+      // each class sizes its workers against what is left of the budget
+      const size_t taken = scr.demand() - demand0;
+      const size_t budget = budget0 > taken ? budget0 - taken : 0;
       EnumArgs args{};
       args.n = n;
       args.ro = g->ro;

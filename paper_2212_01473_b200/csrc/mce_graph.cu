@@ -189,8 +189,10 @@ __global__ void k_edge_keys(const int64_t* __restrict__ edges, int64_t m, int b,
   if (__syncthreads_or(oob) && threadIdx.x == 0) atomicExch(bad, 1);
 }
 
-// both directed keys of every input pair; loops -> all-ones (dropped later)
-__global__ void k_edge_keys_both(const int64_t* __restrict__ edges, int64_t m, int b, int64_t n,
+// both directed keys of every input pair; loops -> all-ones (dropped later).
+// T = int64_t (the reference's edge array) or int32_t (half the ingress bytes)
+template <typename T>
+__global__ void k_edge_keys_both(const T* __restrict__ edges, int64_t m, int b, int64_t n,
                                  uint64_t* __restrict__ keys, int* __restrict__ bad) {
   bool oob = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
@@ -1192,8 +1194,11 @@ int mce_graph_sync_stats(const mce_graph* cg) {
 
 extern "C" {
 
-int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
-                         int edges_on_device, void* stream, mce_graph** out) {
+}  // extern "C"
+
+template <typename T>
+int from_edges_impl(const T* edges, int64_t num_edges, int64_t num_vertices, int edges_on_device,
+                    void* stream, mce_graph** out) {
   mce_prepare_device();
   cudaStream_t s = (cudaStream_t)stream;
   *out = nullptr;
@@ -1205,11 +1210,11 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
   cudaGetDevice(&g->device);
   g->n = num_vertices;
   const int b = bits_for(std::max<int64_t>(num_vertices, 2));
-  const int64_t* d_edges = edges;
-  int64_t* owned = nullptr;
+  const T* d_edges = edges;
+  T* owned = nullptr;
   if (!edges_on_device && num_edges > 0) {
     if (dev_alloc(&owned, 2 * num_edges, s)) { delete g; return -1; }
-    MCE_CHECK(cudaMemcpyAsync(owned, edges, sizeof(int64_t) * 2 * num_edges,
+    MCE_CHECK(cudaMemcpyAsync(owned, edges, sizeof(T) * 2 * num_edges,
                               cudaMemcpyHostToDevice, s));
     d_edges = owned;
   }
@@ -1222,7 +1227,7 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
     int64_t* d_cnt = nullptr;  // [0] unique count, [1] out-of-range flag, [2] last key is a loop
     if (dev_alloc(&keys, dk, s) || dev_alloc(&d_cnt, 3, s)) return -1;
     MCE_CHECK(cudaMemsetAsync(d_cnt, 0, 3 * sizeof(int64_t), s));
-    k_edge_keys_both<<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, num_vertices,
+    k_edge_keys_both<T><<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, b, num_vertices,
                                                          keys, (int*)(d_cnt + 1));
     mce_count_launch();
     MCE_CHECK(cudaGetLastError());
@@ -1259,6 +1264,18 @@ int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_ve
   if (rc) { delete g; return rc; }
   *out = g;
   return 0;
+}
+
+extern "C" {
+
+int mce_graph_from_edges(const int64_t* edges, int64_t num_edges, int64_t num_vertices,
+                         int edges_on_device, void* stream, mce_graph** out) {
+  return from_edges_impl<int64_t>(edges, num_edges, num_vertices, edges_on_device, stream, out);
+}
+
+int mce_graph_from_edges32(const int32_t* edges, int64_t num_edges, int64_t num_vertices,
+                           int edges_on_device, void* stream, mce_graph** out) {
+  return from_edges_impl<int32_t>(edges, num_edges, num_vertices, edges_on_device, stream, out);
 }
 
 int mce_graph_from_csr(const int64_t* row_offsets, const int64_t* col_indices, int64_t n,
@@ -1350,7 +1367,10 @@ void mce_graph_free(mce_graph* g) {
   if (g->split) cudaFreeAsync(g->split, 0);
   if (g->labels) cudaFreeAsync(g->labels, 0);
   if (g->stats_dev) cudaFreeAsync(g->stats_dev, 0);
-  if (g->vhash) cudaFreeAsync(g->vhash, 0);
+  for (int t = 0; t < 2; ++t) {
+    if (g->vhash_tab[t]) cudaFreeAsync(g->vhash_tab[t], 0);
+    if (g->vhash_ev[t]) cudaEventDestroy(g->vhash_ev[t]);
+  }
   if (g->stats_slot) {
     StatsSlot* sl = static_cast<StatsSlot*>(g->stats_slot);
     cudaEventSynchronize(sl->ev);  // its copy must land before the slot is reused

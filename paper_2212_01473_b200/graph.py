@@ -92,6 +92,10 @@ class Graph:
         self._labels = _labels
         self._device_labels = _device_labels
         self._info: dict | None = None
+        # ordering method behind a reordered graph ("parallel" / "exact" are
+        # deterministic, "async" is not); None for graphs not made by
+        # preprocess/reorder.  Sharding across ranks checks it.
+        self.order_method: str | None = None
         if self._dev is None and (self._ro is None or self._ci is None):
             raise ValueError("Graph needs CSR arrays or a device graph")
 
@@ -254,10 +258,11 @@ class DegeneracyOrder:
     (reference graph.py:96-100).  ``position`` may be produced lazily (by
     ``preprocess``, which keeps the permutation on the device)."""
 
-    __slots__ = ("_position", "_degeneracy", "_thunk", "_dthunk")
+    __slots__ = ("_position", "_degeneracy", "_thunk", "_dthunk", "method")
 
     def __init__(self, position: np.ndarray | None, degeneracy: int | None, _thunk=None,
-                 _dthunk=None) -> None:
+                 _dthunk=None, method: str | None = None) -> None:
+        self.method = method
         self._position = position
         self._degeneracy = None if degeneracy is None else int(degeneracy)
         self._thunk = _thunk
@@ -292,23 +297,32 @@ def _from_device(n: int, h: ctypes.c_void_p, labels: np.ndarray | None = None) -
 def from_edges(edges: Iterable[tuple[int, int]] | np.ndarray, num_vertices: int) -> Graph:
     """Canonical graph from compacted vertex pairs, built on the GPU
     (reference graph.py:103-129): self-loops dropped, duplicates merged,
-    both directions stored, rows ascending."""
-    arr = np.ascontiguousarray(
-        np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges,
-                   dtype=np.int64).reshape(-1, 2))
+    both directions stored, rows ascending.  An int32 array is shipped as
+    is (``mce_graph_from_edges32``: half the host->device bytes); anything
+    else as int64, like the reference."""
+    if isinstance(edges, np.ndarray) and edges.dtype == np.int32:
+        arr = np.ascontiguousarray(edges.reshape(-1, 2))
+        entry = "mce_graph_from_edges32"
+    else:
+        arr = np.ascontiguousarray(
+            np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges,
+                       dtype=np.int64).reshape(-1, 2))
+        entry = "mce_graph_from_edges"
     h = ctypes.c_void_p()  # ids outside [0, n) are rejected on the device (ValueError)
-    _lib.check(_lib.lib().mce_graph_from_edges(_lib.ptr(arr), len(arr), int(num_vertices), 0,
-                                               None, ctypes.byref(h)), "mce_graph_from_edges")
+    _lib.check(getattr(_lib.lib(), entry)(_lib.ptr(arr), len(arr), int(num_vertices), 0,
+                                          None, ctypes.byref(h)), entry)
     return _from_device(num_vertices, h)
 
 
 def from_device_edges(edges_dev, num_edges: int, num_vertices: int, stream=None) -> Graph:
     """Canonical graph from an edge buffer already in device memory
-    (int64 pairs; e.g. a torch CUDA tensor or mce_gen_rmat output)."""
+    (int64 or int32 pairs; e.g. a torch CUDA tensor or mce_gen_rmat output)."""
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib().mce_graph_from_edges(_lib.ptr(edges_dev), int(num_edges),
-                                               int(num_vertices), 1, stream, ctypes.byref(h)),
-               "mce_graph_from_edges")
+    dt = getattr(edges_dev, "dtype", None)
+    entry = "mce_graph_from_edges32" if str(dt) in ("torch.int32", "int32") else \
+        "mce_graph_from_edges"
+    _lib.check(getattr(_lib.lib(), entry)(_lib.ptr(edges_dev), int(num_edges),
+                                          int(num_vertices), 1, stream, ctypes.byref(h)), entry)
     return _from_device(num_vertices, h)
 
 
@@ -365,7 +379,7 @@ def degeneracy_order(g: Graph, method: str = "async") -> DegeneracyOrder:
         _lib.check(_lib.lib().mce_degeneracy_order(g.device.handle, ORDER_METHODS[method],
                                                    _lib.ptr(pos), 0, ctypes.byref(d), None),
                    "mce_degeneracy_order")
-    return DegeneracyOrder(pos, int(d.value))
+    return DegeneracyOrder(pos, int(d.value), method=method)
 
 
 def reorder(g: Graph, order: DegeneracyOrder) -> Graph:
@@ -382,7 +396,9 @@ def reorder(g: Graph, order: DegeneracyOrder) -> Graph:
     base = g.labels if g.labels is not None else np.arange(n, dtype=np.int64)
     labels = np.empty(n, dtype=np.int64)
     labels[pos] = base
-    return _from_device(n, h, labels)
+    g2 = _from_device(n, h, labels)
+    g2.order_method = order.method
+    return g2
 
 
 def stats(g: Graph, order: DegeneracyOrder) -> GraphStats:
@@ -407,8 +423,9 @@ def preprocess(g: Graph, method: str = "async") -> tuple[Graph, DegeneracyOrder,
         raise ValueError(f"unknown ordering method {method!r}")
     n = g.num_vertices
     if n == 0:
-        order = DegeneracyOrder(np.empty(0, dtype=np.int64), 0)
+        order = DegeneracyOrder(np.empty(0, dtype=np.int64), 0, method=method)
         g2 = from_edges(np.empty((0, 2), dtype=np.int64), 0)
+        g2.order_method = method
         return g2, order, stats(g2, order)
     h = ctypes.c_void_p()
     # no degeneracy out-parameter: the call returns once its work is queued;
@@ -416,6 +433,7 @@ def preprocess(g: Graph, method: str = "async") -> tuple[Graph, DegeneracyOrder,
     _lib.check(_lib.lib().mce_preprocess(g.device.handle, ORDER_METHODS[method], None,
                                          None, ctypes.byref(h)), "mce_preprocess")
     g2 = Graph(n, _device=_DeviceGraph(h), _device_labels=True)
+    g2.order_method = method
     base = g.labels
 
     def position() -> np.ndarray:
@@ -428,6 +446,7 @@ def preprocess(g: Graph, method: str = "async") -> tuple[Graph, DegeneracyOrder,
         info = g2.device_info()
         return info["nnz"] // 2, info["max_degree"], info["max_later"]
 
-    order = DegeneracyOrder(None, None, _thunk=position, _dthunk=lambda: device_stats()[2])
+    order = DegeneracyOrder(None, None, _thunk=position, _dthunk=lambda: device_stats()[2],
+                            method=method)
     st = GraphStats(n, _thunk=device_stats)
     return g2, order, st

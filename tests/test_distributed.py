@@ -67,8 +67,10 @@ def test_allreduce_sums_counts_histograms_and_wraps_the_hash(tmp_path):
     assert a == b
     assert (a.cliques, a.nodes, a.donations) == (21, 300, 1)
     assert a.hash == (MASK64 - 5 + 11) & MASK64 == 5
-    # sizes beyond the packed histogram fold into its last slot
-    assert a.hist[3] == 3 and sum(a.hist.values()) == 7
+    # every size is reduced in its own slot (RMAT cores reach sizes > 100)
+    assert a.hist == {3: 3, 200: 4}
+    with pytest.raises(ValueError):
+        ShardResult(1, 1, 0, 0, {5000: 1}).pack()
 
 
 # ---------------------------------------------------------------- work stealing
@@ -140,14 +142,25 @@ def test_stealing_rejects_bad_chunking():
 
 # ---------------------------------------------------------------- static shards
 
-def test_static_shards_partition_the_roots_exactly():
-    """Per-shard oracle runs over shard_bounds(r, world) sum to the whole run:
-    same count, node total, histogram and clique-set hash."""
-    from oracle import oracle
+def _with_big_clique(n=400, p=0.05, k=130, seed=7):
+    """G(n, p) plus a planted k-clique (k >= 128: sizes past the old 128-slot
+    histogram) on random vertices."""
     from paper_2212_01473_b200 import generate
 
-    edges = generate.gnp_edges(400, 0.05, seed=7)
-    ro, ci = oracle.from_edges(edges, 400)
+    edges = generate.gnp_edges(n, p, seed=seed)
+    members = np.random.default_rng(seed).choice(n, size=k, replace=False)
+    iu, ju = np.triu_indices(k, 1)
+    return np.concatenate([edges, np.column_stack((members[iu], members[ju]))]), n
+
+
+def test_static_shards_partition_the_roots_exactly():
+    """Per-shard oracle runs over shard_bounds(r, world) sum to the whole run:
+    same count, node total, histogram and clique-set hash -- including a
+    clique of size >= 128."""
+    from oracle import oracle
+
+    edges, n = _with_big_clique()
+    ro, ci = oracle.from_edges(edges, n)
     pos, d = oracle.degeneracy_order(ro, ci)
     ro2, ci2 = oracle.reorder(ro, ci, pos)
     whole = oracle.enumerate_cliques(ro2, ci2, degeneracy=d, threads=1)
@@ -160,5 +173,89 @@ def test_static_shards_partition_the_roots_exactly():
         tot = combine(parts)
         assert tot.cliques == whole["count"] and tot.nodes == whole["nodes"]
         assert f"{tot.hash:016x}" == whole["hash"] and tot.hist == whole["hist"]
+    assert max(whole["hist"]) >= 128
     with pytest.raises(ValueError):
         shard_bounds(2, 2)
+
+
+def _labels(pos):
+    """Original id of every reordered vertex: the clique hash over labels
+    does not depend on the ordering."""
+    lab = np.empty(len(pos), dtype=np.int64)
+    lab[pos] = np.arange(len(pos), dtype=np.int64)
+    return lab
+
+
+def _gloo_shard_worker(rank, port, out_dir):
+    """Each rank orders the graph itself (deterministic bucket peel, the
+    numpy restatement of method='parallel'), enumerates its shard with the
+    oracle and joins the one all-reduce."""
+    from oracle import oracle
+
+    _init(rank, port)
+    try:
+        edges, n = _with_big_clique()
+        ro, ci = oracle.from_edges(edges, n)
+        pos, d = oracle.bucket_peel_order(ro, ci)
+        ro2, ci2 = oracle.reorder(ro, ci, pos)
+        o = oracle.enumerate_cliques(ro2, ci2, degeneracy=d, threads=1, labels=_labels(pos),
+                                     **shard_bounds(rank, WORLD))
+        tot = allreduce_result(ShardResult(o["count"], o["nodes"], 0, int(o["hash"], 16), o["hist"]))
+        np.save(os.path.join(out_dir, f"shard{rank}.npy"), tot.pack())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_shards_with_per_rank_ordering_sum_to_the_whole(tmp_path):
+    from oracle import oracle
+
+    _spawn(_gloo_shard_worker, str(tmp_path))
+    edges, n = _with_big_clique()
+    ro, ci = oracle.from_edges(edges, n)
+    pos, d = oracle.degeneracy_order(ro, ci)
+    whole = oracle.enumerate_cliques(*oracle.reorder(ro, ci, pos), degeneracy=d, threads=1,
+                                     labels=_labels(pos))
+    for r in range(WORLD):
+        tot = ShardResult.unpack(np.load(tmp_path / f"shard{r}.npy"))
+        assert tot.cliques == whole["count"] and tot.hist == whole["hist"]
+        assert f"{tot.hash:016x}" == whole["hash"]
+    assert max(tot.hist) >= 128
+
+
+def test_shards_of_two_different_orderings_do_not_partition():
+    """Why sharding needs ONE ordering: shard 0 of one valid degeneracy order
+    plus shard 1 of another (both with the reference's degeneracy) miss or
+    double-count cliques -- the failure the async peel's run-to-run tie-breaks
+    would cause; and run_shard refuses an async-ordered graph at world > 1."""
+    from oracle import oracle
+    from paper_2212_01473_b200 import generate
+    from paper_2212_01473_b200.distributed import check_shardable
+
+    edges = generate.gnp_edges(400, 0.05, seed=0)
+    ro, ci = oracle.from_edges(edges, 400)
+    pos_a, d = oracle.degeneracy_order(ro, ci)
+    pos_b, d_b = oracle.bucket_peel_order(ro, ci)
+    assert d == d_b and not np.array_equal(pos_a, pos_b)
+    whole = oracle.enumerate_cliques(*oracle.reorder(ro, ci, pos_a), degeneracy=d, threads=1,
+                                     labels=_labels(pos_a))
+    s0 = oracle.enumerate_cliques(*oracle.reorder(ro, ci, pos_a), degeneracy=d, threads=1,
+                                  labels=_labels(pos_a), **shard_bounds(0, 2))
+    s1 = oracle.enumerate_cliques(*oracle.reorder(ro, ci, pos_b), degeneracy=d, threads=1,
+                                  labels=_labels(pos_b), **shard_bounds(1, 2))
+    mixed = combine([ShardResult(o["count"], o["nodes"], 0, int(o["hash"], 16), o["hist"])
+                     for o in (s0, s1)])
+    assert f"{mixed.hash:016x}" != whole["hash"]
+    # each ordering on its own still shards exactly
+    s1a = oracle.enumerate_cliques(*oracle.reorder(ro, ci, pos_a), degeneracy=d, threads=1,
+                                   labels=_labels(pos_a), **shard_bounds(1, 2))
+    same = combine([ShardResult(o["count"], o["nodes"], 0, int(o["hash"], 16), o["hist"])
+                    for o in (s0, s1a)])
+    assert f"{same.hash:016x}" == whole["hash"] and same.cliques == whole["count"]
+
+    class G:
+        order_method = "async"
+    with pytest.raises(ValueError):
+        check_shardable(G(), 2)
+    check_shardable(G(), 1)
+    G.order_method = "parallel"
+    check_shardable(G(), 2)

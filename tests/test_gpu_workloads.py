@@ -113,6 +113,34 @@ def test_planted_full_l1_equals_l2_and_shards_sum():
     assert tot.nodes == whole.nodes_total
 
 
+@pytest.mark.parametrize("name", ["ba200k", "planted1m"])
+def test_per_rank_orderings_shard_exactly(name):
+    """The N>1 code path as two ranks run it: each rank builds ITS OWN
+    ordering (preprocess_for_shards: the deterministic parallel peel at
+    world > 1) and enumerates its shard through run_shard; the two partial
+    results must add up to the whole run (count, node total, histogram,
+    hash).  With the async peel (the old per-rank default) two independent
+    orderings differ, and run_shard refuses them at world > 1."""
+    from paper_2212_01473_b200.distributed import preprocess_for_shards, run_shard
+
+    edges, n = generate.workload_edges(name)
+    cfg = RunConfig()
+    whole_g, _, whole_st = preprocess(from_edges(edges, n), method="parallel")
+    whole = run(whole_g, whole_st, cfg)
+    parts = []
+    for rank in range(2):
+        g2, order, st = preprocess_for_shards(from_edges(edges, n), 2)  # independent per rank
+        assert g2.order_method == "parallel"
+        _, part = run_shard(g2, st, cfg, rank, 2)
+        parts.append(part)
+    tot = combine(parts)
+    assert (tot.cliques, tot.hash, tot.hist, tot.nodes) == \
+        (whole.clique_count, whole.clique_hash, whole.size_histogram, whole.nodes_total)
+    ga, _, sta = preprocess(from_edges(edges, n), method="async")
+    with pytest.raises(ValueError):
+        run_shard(ga, sta, cfg, 0, 2)
+
+
 def test_from_edges_rejects_out_of_range_ids_on_device():
     for bad in ([(0, 5)], [(-1, 2)], [(0, 1), (2, 3)]):
         with pytest.raises(ValueError):

@@ -50,6 +50,7 @@
 namespace {
 
 constexpr int HIST_SMEM = 128;
+constexpr int CMP_WORDS = 256;  // per-warp compact_run scratch: 64 + 64 ints, 64 x 8-byte rows
 constexpr int HIST_MAX = MCE_HIST_MAX;
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int ROOT_STRIPES = 32;  // root-claim counters (<= 32: one per lane in phase2())
@@ -138,6 +139,7 @@ struct EnumArgs {
   int xrows_partial_max;  // partial mode: X rows only for roots with |X| <= this
   const uint32_t* heavy_rows;  // X rows of the heavy-X roots (k_heavy_xrows), per slot
   const int64_t* heavy_off;    // word offset of slot h's rows (stride |X| of the root)
+  int compact;                 // run small subtrees on the register copy (compact_run); 0: off
 };
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* a, int len, int32_t key) {
@@ -239,6 +241,9 @@ struct Worker {
   int32_t* lpx;
   int32_t* rpath;
   uint64_t* hsum;
+  int32_t* cu;      // compact_run scratch (shared memory): U members
+  int32_t* ctok;    //   X_X tokens during a partition
+  uint32_t* cbuf;   //   X_X rows during a partition (64 x 8 bytes)
   const int32_t* root_x;
   int np = 0, nx = 0;
   int64_t origin = 0;
@@ -256,9 +261,11 @@ struct Worker {
   bool phase2_seen = false;
 
   __device__ Worker(const EnumArgs& args, int lane_, int wid_, uint32_t* smem_rows,
-                    int32_t* smem_plist, uint32_t* smem_p, unsigned int* smem_hist)
+                    int32_t* smem_plist, uint32_t* smem_p, unsigned int* smem_hist,
+                    int32_t* smem_cmp)
       : a(args), lane(lane_), wid(wid_), sP(smem_p), sXP(smem_p + SPW), sBR(smem_p + 2 * SPW),
-        s_hist(smem_hist) {
+        s_hist(smem_hist), cu(smem_cmp), ctok(smem_cmp + 64),
+        cbuf(reinterpret_cast<uint32_t*>(smem_cmp + 128)) {
     if (ROWS_SMEM) {
       rowsT = smem_rows;
       plist = smem_plist;
@@ -843,9 +850,28 @@ struct Worker {
   // donate the branch (v, childP, childXP) to an idle worker (scheduler.py:417-438)
   __device__ bool try_donate(const B& childP, const B& childXP, int v, int32_t gv, int live,
                              int rlen) {
+    const int rid = claim_receiver();
+    if (rid < 0) return false;
+    // receiver's X_X: the live tokens adjacent to v, in prefix order
+    int32_t* rx = a.xx + (size_t)rid * a.xcap;
+    int k = 0;
+    const unsigned lt = (1u << lane) - 1;
+    for (int base = 0; base < live; base += 32) {
+      int i = base + lane;
+      bool keep = (i < live) && xx_adjacent(xx[i], v, gv);
+      unsigned km = __ballot_sync(FULLMASK, keep);
+      if (keep) rx[k + __popc(km & lt)] = xx[i];
+      k += __popc(km);
+    }
+    send_branch(rid, childP, childXP, gv, rlen, k);
+    return true;
+  }
+
+  // claim an idle worker off the worker list (-1: none parked)
+  __device__ int claim_receiver() {
     int rid = -1;
     const unsigned long long st = *(volatile unsigned long long*)&a.wl->state;
-    if ((st >> 32) == 0) return false;  // nobody parked
+    if ((st >> 32) == 0) return -1;  // nobody parked
     const int nwords = (a.num_workers + 31) >> 5;
     const int start = (wid * 7) % nwords;
     for (int base = 0; base < nwords && rid < 0; base += 32) {
@@ -869,22 +895,16 @@ struct Worker {
         rid = __shfl_sync(FULLMASK, claimed, 0);
       }
     }
-    rid = __shfl_sync(FULLMASK, rid, 0);
-    if (rid < 0) return false;
+    return __shfl_sync(FULLMASK, rid, 0);
+  }
+
+  // hand the claimed worker `rid` the branch (its X_X tokens, nxx of them,
+  // are already in its xx buffer): R path, P / X_P bitsets, the root's rows
+  __device__ void send_branch(int rid, const B& childP, const B& childXP, int32_t gv, int rlen,
+                              int nxx) {
     Mailbox* mb = a.mbox + rid;
     uint32_t* mbits = a.mbits + (size_t)rid * 2 * W;
-    int32_t* rx = a.xx + (size_t)rid * a.xcap;
     int32_t* rr = a.rpath + (size_t)rid * (a.levels + 2);
-    // receiver's X_X: the live tokens adjacent to v, in prefix order
-    int k = 0;
-    const unsigned lt = (1u << lane) - 1;
-    for (int base = 0; base < live; base += 32) {
-      int i = base + lane;
-      bool keep = (i < live) && xx_adjacent(xx[i], v, gv);
-      unsigned km = __ballot_sync(FULLMASK, keep);
-      if (keep) rx[k + __popc(km & lt)] = xx[i];
-      k += __popc(km);
-    }
     for (int i = lane; i < rlen; i += 32) rr[i] = rpath[i];
 #pragma unroll
     for (int q = 0; q < K; ++q) {
@@ -904,7 +924,7 @@ struct Worker {
       rr[rlen] = gv;
       mb->origin = origin;
       mb->rlen = rlen + 1;
-      mb->nxx = k;
+      mb->nxx = nxx;
       mb->owner = owner_wid;
       mb->np = np;
       mb->nx = nx;
@@ -915,7 +935,6 @@ struct Worker {
     __syncwarp();
     if (lane == 0) atomicExch(&a.wl_wake[rid], 1);
     don_made++;
-    return true;
   }
 
   // park on the worker list until donated to (true) or terminated (false)
@@ -952,6 +971,401 @@ struct Worker {
     return got != 0;
   }
 
+  // ---------------------------------------------------------------- compact subtrees
+  // Below a node whose candidate set U = P | X_P has at most CW (32 or 64)
+  // members and whose live X_X prefix holds at most CW tokens, the rest of
+  // the subtree runs on a re-indexed copy held in registers:
+  //  * slot s = the s-th member of U in ascending local id, so the pivot's
+  //    smallest-id tie-break and the ascending branch order are unchanged;
+  //  * lane l holds the rows (restricted to U) of slots l and l + 32, and
+  //    the rows and tokens of the live X_X members at prefix positions l and
+  //    l + 32 -- the stable partition permutes them between lanes;
+  //  * P, X_P, the branch and non-leaf sets are warp-uniform CW-bit masks;
+  //  * the DFS frames live in lane registers (frame d in lane d & 31).
+  // Pivot rule, leaf batch, X_X partition, node accounting and donation
+  // conditions are traverse()'s, so the traversal tree is unchanged; a
+  // branch donated from here is handed over in the wide (root-local) form.
+  template <typename M>
+  __device__ __forceinline__ static int popcm(M x) {
+    if (sizeof(M) == 8) return __popcll((unsigned long long)x);
+    return __popc((unsigned)x);
+  }
+  template <typename M>
+  __device__ __forceinline__ static int ffsm(M x) {
+    if (sizeof(M) == 8) return __ffsll((long long)x) - 1;
+    return __ffs((unsigned)x) - 1;
+  }
+  template <typename M>
+  __device__ __forceinline__ static M shflm(M x, int src) {
+    if (sizeof(M) == 8) return (M)__shfl_sync(FULLMASK, (unsigned long long)x, src);
+    return (M)__shfl_sync(FULLMASK, (unsigned)x, src);
+  }
+  template <typename M>
+  __device__ __forceinline__ static M ballotm(bool p, int h) {
+    return (M)((unsigned long long)__ballot_sync(FULLMASK, p) << (32 * h));
+  }
+  template <typename M>
+  __device__ __forceinline__ static M reduce_orm(M x) {
+    M r = (M)__reduce_or_sync(FULLMASK, (unsigned)x);
+    if (sizeof(M) == 8)
+      r |= (M)((unsigned long long)__reduce_or_sync(FULLMASK, (unsigned)((unsigned long long)x >> 32)) << 32);
+    return r;
+  }
+
+  // eligible when |P | X_P| and the live X_X prefix fit CW bits and every live
+  // X_X member has its row (X rows built, or none live)
+  __device__ int compact_width(const B& P, const B& XP, int live) const {
+    if (!a.compact || live > 64 || (live > 0 && !(XROWS && xr))) return 0;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) c += __popc(P.w[k] | XP.w[k]);
+    c = __reduce_add_sync(FULLMASK, c);
+    if (c > 64) return 0;
+    return (c <= 32 && live <= 32) ? 32 : 64;
+  }
+
+  template <typename M>
+  __device__ __forceinline__ void compact_run(const B& Pw, const B& XPw, int live, int rlen, int& below,
+                              uint64_t hs) {
+    constexpr int H = (int)sizeof(M) / 4;  // slots per lane
+    const unsigned lt = (1u << lane) - 1;
+    // ---- U members (ascending local id), bit 31: member of P
+    int nu = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t uw = valid(k, lane) ? (Pw.w[k] | XPw.w[k]) : 0u;
+      const uint32_t pw = valid(k, lane) ? Pw.w[k] : 0u;
+      const int c = __popc(uw);
+      int incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, incl, d);
+        if (lane >= d) incl += t;
+      }
+      int pos = nu + incl - c;
+      const int wid_ = k * 32 + lane;
+      for (uint32_t t = uw; t; t &= t - 1) {
+        const int b = __ffs(t) - 1;
+        cu[pos++] = ((wid_ << 5) + b) | (int)(((pw >> b) & 1u) << 31);
+      }
+      nu += __shfl_sync(FULLMASK, incl, 31);
+    }
+    __syncwarp();
+    const M umask = nu >= (int)(8 * sizeof(M)) ? ~(M)0 : (((M)1 << nu) - 1);
+    const bool contig = (cu[nu - 1] & 0x7fffffff) == nu - 1;  // U = {0 .. nu-1}
+    const int live0 = live;
+    M row[H], xrow[H];
+    int cid[H], tok[H];
+    int32_t gvs[H];
+    uint64_t vh[H];
+    M P = 0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int s = lane + 32 * h;
+      const bool sv = s < nu;
+      const int e = sv ? cu[s] : 0;
+      cid[h] = e & 0x7fffffff;
+      P |= ballotm<M>(sv && e < 0, h);
+      gvs[h] = sv ? plist[cid[h]] : 0;
+      vh[h] = sv ? a.vhash[gvs[h]] : 0ull;
+      const int p = lane + 32 * h;
+      tok[h] = p < live ? xx[p] : 0;
+      row[h] = 0;
+      xrow[h] = 0;
+    }
+    M XP = umask & ~P;
+    if (contig) {  // the rows' first words are already indexed by slot
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int s = lane + 32 * h;
+        const int p = lane + 32 * h;
+        if (s < nu) {
+          M r = (M)rowsT[cid[h]];
+          if (H == 2 && W >= 2) r |= (M)((unsigned long long)rowsT[CAPP + cid[h]] << 32);
+          row[h] = r & umask;
+        }
+        if (p < live) {
+          M r = (M)xrowsT[tok[h]];
+          if (H == 2 && W >= 2) r |= (M)((unsigned long long)xrowsT[(size_t)xstride + tok[h]] << 32);
+          xrow[h] = r & umask;
+        }
+      }
+    } else {  // gather bit u_t of every row word, one load per distinct word
+      int curw = -1;
+      uint32_t rw[H], xw[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) rw[h] = xw[h] = 0;
+      for (int t = 0; t < nu; ++t) {
+        const int u = cu[t] & 0x7fffffff;
+        const int w = u >> 5;
+        if (w != curw) {
+          curw = w;
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const int s = lane + 32 * h;
+            rw[h] = s < nu ? rowsT[w * CAPP + cid[h]] : 0u;
+            xw[h] = s < live ? xrowsT[(size_t)w * xstride + tok[h]] : 0u;
+          }
+        }
+        const int b = u & 31;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          row[h] |= (M)((rw[h] >> b) & 1u) << t;
+          xrow[h] |= (M)((xw[h] >> b) & 1u) << t;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- DFS frames in lane registers
+    M fP[H], fXP[H], fBR[H], fNL[H];
+    int flive[H];
+    uint64_t fhs[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      fP[h] = fXP[h] = fBR[h] = fNL[h] = 0;
+      flive[h] = 0;
+      fhs[h] = 0;
+    }
+    int depth = 0;
+    M BR = 0, NL = 0;
+    bool fresh = true;
+    for (;;) {
+      if (fresh) {
+        fresh = false;
+        // pivot (bk.py:82-110): max |N(c) & P| over P | X_P, ties to the smallest slot
+        const M cand = P | XP;
+        unsigned key = 0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int s = lane + 32 * h;
+          if ((cand >> s) & 1) {
+            const unsigned k2 = ((unsigned)(popcm(row[h] & P) + 1) << 7) | (unsigned)(127 - s);
+            key = k2 > key ? k2 : key;
+          }
+        }
+        const unsigned km = __reduce_max_sync(FULLMASK, key);
+        const int ps = 127 - (int)(km & 127);
+        M prow = shflm(H == 2 && ps >= 32 ? row[H - 1] : row[0], ps & 31);
+        if (PIVOT_XX && live > 0) {  // X_X rows win only when strictly better, first in prefix order
+          unsigned xk = 0;
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const int p = lane + 32 * h;
+            if (p < live) {
+              const unsigned k2 = ((unsigned)(popcm(xrow[h] & P) + 1) << 7) | (unsigned)(127 - p);
+              xk = k2 > xk ? k2 : xk;
+            }
+          }
+          const unsigned xm = __reduce_max_sync(FULLMASK, xk);
+          if ((xm >> 7) > (km >> 7)) {
+            const int pp = 127 - (int)(xm & 127);
+            prow = shflm(H == 2 && pp >= 32 ? xrow[H - 1] : xrow[0], pp & 31);
+          }
+        }
+        BR = P & ~prow;
+        // leaf batch (see leaf_batch): every branch whose child P is empty
+        M xxadj = 0;
+        if (live > 0) {
+          M o = 0;
+#pragma unroll
+          for (int h = 0; h < H; ++h)
+            if (lane + 32 * h < live) o |= xrow[h];
+          xxadj = reduce_orm(o);
+        }
+        const int size = rlen + 1;
+        M leafm = 0, maxm = 0;
+        unsigned long long hl = 0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int s = lane + 32 * h;
+          bool leaf = false, xcl = false;
+          if ((BR >> s) & 1) {
+            const M before = BR & (((M)1 << s) - 1);
+            leaf = (row[h] & (P & ~before)) == 0;
+            xcl = leaf && (row[h] & (XP | before)) == 0 && !((xxadj >> s) & 1);
+          }
+          leafm |= ballotm<M>(leaf, h);
+          maxm |= ballotm<M>(xcl, h);
+          if (xcl) hl += mce_mix64(hs + vh[h] + (uint64_t)size * MCE_SIZE_SALT);
+        }
+        nodes += popcm(leafm);
+        NL = BR & ~leafm;
+        if (maxm) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) hl += __shfl_xor_sync(FULLMASK, hl, o);
+          const int cnt = popcm(maxm);
+          if (lane == 0) {
+            cliques += cnt;
+            hash += hl;
+            if ((unsigned long long)size > max_size) max_size = size;
+            hist_add(size, (unsigned)cnt);
+          }
+          if (a.collect_cap > 0) {
+            for (M t = maxm; t; t &= t - 1) {
+              const int sv = ffsm(t);
+              collect_clique(size, __shfl_sync(FULLMASK, H == 2 && sv >= 32 ? gvs[H - 1] : gvs[0], sv & 31));
+            }
+          }
+        }
+      }
+      const int v = NL ? ffsm(NL) : -1;
+      if (v < 0) {
+        if (depth == 0) break;
+        depth--;
+        rlen--;
+        const int fl = depth & 31, fh = depth >> 5;
+        P = shflm(H == 2 && fh ? fP[H - 1] : fP[0], fl);
+        XP = shflm(H == 2 && fh ? fXP[H - 1] : fXP[0], fl);
+        BR = shflm(H == 2 && fh ? fBR[H - 1] : fBR[0], fl);
+        NL = shflm(H == 2 && fh ? fNL[H - 1] : fNL[0], fl);
+        live = __shfl_sync(FULLMASK, H == 2 && fh ? flive[H - 1] : flive[0], fl);
+        hs = __shfl_sync(FULLMASK, H == 2 && fh ? fhs[H - 1] : fhs[0], fl);
+        if (NL) below--;
+        continue;
+      }
+      // move v and the (leaf) branches before it from P to X_P
+      const M bit = (M)1 << v;
+      const M mv = (BR & (bit - 1)) | bit;
+      BR &= ~mv;
+      NL &= ~mv;
+      P &= ~mv;
+      XP |= mv;
+      const int vl = v & 31;
+      const bool vh2 = H == 2 && v >= 32;
+      const M rowv = shflm(vh2 ? row[H - 1] : row[0], vl);
+      const M childP = P & rowv;
+      const int32_t gv = __shfl_sync(FULLMASK, vh2 ? gvs[H - 1] : gvs[0], vl);
+      const uint64_t vhv = __shfl_sync(FULLMASK, vh2 ? vh[H - 1] : vh[0], vl);
+      if (a.worker_list_on && (popcm(childP) >= a.min_p || (a.min_x > 0 && live >= a.min_x)) &&
+          below > 0 && NL != 0 && phase2()) {
+        if (donate_compact<M, H>(childP, XP & rowv, v, gv, live, rlen, cid, nu, xrow, tok)) continue;
+      }
+      // stable partition of the live X_X prefix by adjacency to v (xsets.py:55-82)
+      int kept = 0;
+      if (live > 0) {
+        unsigned kb[H], db[H];
+        bool keep[H], ok[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int p = lane + 32 * h;
+          ok[h] = p < live;
+          keep[h] = ok[h] && ((xrow[h] >> v) & 1);
+          kb[h] = __ballot_sync(FULLMASK, keep[h]);
+          db[h] = __ballot_sync(FULLMASK, ok[h] && !keep[h]);
+          kept += __popc(kb[h]);
+        }
+        int kbase = 0, dbase = kept;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          int dst = -1;
+          if (keep[h]) dst = kbase + __popc(kb[h] & lt);
+          else if (ok[h]) dst = dbase + __popc(db[h] & lt);
+          kbase += __popc(kb[h]);
+          dbase += __popc(db[h]);
+          if (dst >= 0) {
+            cbuf_as<M>()[dst] = xrow[h];
+            ctok[dst] = tok[h];
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int p = lane + 32 * h;
+          if (p < live) {
+            xrow[h] = cbuf_as<M>()[p];
+            tok[h] = ctok[p];
+          }
+        }
+        __syncwarp();
+      }
+      {  // push the frame of this level
+        const int fl = depth & 31, fh = depth >> 5;
+        if (lane == fl) {
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            if (h == fh) {
+              fP[h] = P;
+              fXP[h] = XP;
+              fBR[h] = BR;
+              fNL[h] = NL;
+              flive[h] = live;
+              fhs[h] = hs;
+            }
+          }
+        }
+      }
+      if (NL) below++;
+      depth++;
+      live = kept;
+      XP &= rowv;
+      P = childP;
+      if (lane == 0) rpath[rlen] = gv;
+      hs += vhv;
+      rlen++;
+      nodes++;
+      fresh = true;
+    }
+    // the X_X prefix order this subtree left behind (the reference partitions
+    // in place and never restores: the enclosing levels see it)
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int p = lane + 32 * h;
+      if (p < live0) xx[p] = tok[h];
+    }
+    __syncwarp();
+  }
+
+  template <typename M>
+  __device__ __forceinline__ M* cbuf_as() const { return reinterpret_cast<M*>(cbuf); }
+
+  // hand the compact branch (childP, childXP over slots) to an idle worker
+  // in the wide form: slots mapped back to root-local ids, the live X_X
+  // tokens adjacent to v in the current prefix order
+  template <typename M, int H>
+  __device__ __forceinline__ bool donate_compact(M childP, M childXP, int v, int32_t gv, int live, int rlen,
+                                 const int (&cid)[H], int nu, const M (&xrow)[H],
+                                 const int (&tok)[H]) {
+    const unsigned long long st = *(volatile unsigned long long*)&a.wl->state;
+    if ((st >> 32) == 0) return false;  // nobody parked: skip the expansion
+    for (int i = lane; i < W; i += 32) {
+      sP[i] = 0;
+      sXP[i] = 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int s = lane + 32 * h;
+      if (s < nu) {
+        const int u = cid[h];
+        if ((childP >> s) & 1) atomicOr(&sP[u >> 5], 1u << (u & 31));
+        if ((childXP >> s) & 1) atomicOr(&sXP[u >> 5], 1u << (u & 31));
+      }
+    }
+    __syncwarp();
+    B cP, cXP;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      cP.w[k] = valid(k, lane) ? sP[word(k)] : 0u;
+      cXP.w[k] = valid(k, lane) ? sXP[word(k)] : 0u;
+    }
+    __syncwarp();
+    const int rid = claim_receiver();
+    if (rid < 0) return false;
+    int32_t* rx = a.xx + (size_t)rid * a.xcap;
+    const unsigned lt = (1u << lane) - 1;
+    int k = 0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int p = lane + 32 * h;
+      const bool keep = p < live && ((xrow[h] >> v) & 1);
+      const unsigned km = __ballot_sync(FULLMASK, keep);
+      if (keep) rx[k + __popc(km & lt)] = tok[h];
+      k += __popc(km);
+    }
+    send_branch(rid, cP, cXP, gv, rlen, k);
+    return true;
+  }
+
   // ---------------------------------------------------------------- DFS
   // frame: P, X_P, remaining branches BR, remaining non-leaf branches NL
   __device__ __forceinline__ void push(int depth, const B& P, const B& XP, const B& BR,
@@ -982,7 +1396,7 @@ struct Worker {
   // Leaves are settled per node by leaf_batch; the loop walks the non-leaf
   // branches in the reference's order, applying the P -> X_P moves of the
   // leaf branches that precede each one.
-  __device__ void traverse(B P, B XP, int nxx, int rlen, bool root_sorted) {
+  __device__ __forceinline__ void traverse(B P, B XP, int nxx, int rlen, bool root_sorted) {
     uint64_t hs = 0;
     for (int i = 0; i < rlen; ++i) hs += a.vhash[rpath[i]];
     if (!any(P)) {  // scheduler.py:300-304
@@ -996,6 +1410,7 @@ struct Worker {
       lpx[0] = nxx;
       hsum[rlen] = hs;
     }
+    __syncwarp();
     int live = nxx;
     nodes++;
     B BR, NL;
@@ -1004,8 +1419,17 @@ struct Worker {
     unsigned long long xsorted = root_sorted ? 1ull : 0ull;
     for (;;) {
       if (fresh) {
-        pivot_branches(P, XP, live, BR);
-        leaf_batch(P, XP, BR, live, rlen, NL, depth < 64 && ((xsorted >> depth) & 1ull));
+        const int cw = compact_width(P, XP, live);
+        if (cw) {  // the whole subtree below this node, on the register copy
+          const uint64_t hs0 = hsum[rlen];
+          if (cw == 32) compact_run<uint32_t>(P, XP, live, rlen, below, hs0);
+          else compact_run<unsigned long long>(P, XP, live, rlen, below, hs0);
+#pragma unroll
+          for (int k = 0; k < K; ++k) NL.w[k] = 0;
+        } else {
+          pivot_branches(P, XP, live, BR);
+          leaf_batch(P, XP, BR, live, rlen, NL, depth < 64 && ((xsorted >> depth) & 1ull));
+        }
         fresh = false;
       }
       const int v = first(NL);
@@ -1125,9 +1549,9 @@ struct Worker {
     return kept;
   }
 
-  __device__ void run_root(int64_t r) {
+  // level-0 state of root r (build its induced rows first); returns the R length
+  __device__ int prepare_root(int64_t r, B& P, B& XP, int& nxx) {
     const int nr = build(r);
-    B P, XP;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       uint32_t x = 0;
@@ -1139,8 +1563,8 @@ struct Worker {
       P.w[k] = x;
       XP.w[k] = 0u;
     }
-    const int nxx = init_tokens();
-    traverse(P, XP, nxx, nr, true);
+    nxx = init_tokens();
+    return nr;
   }
 
   // Take over the root of a donated branch from its owner's buffers (no
@@ -1186,20 +1610,20 @@ struct Worker {
     __syncwarp();
   }
 
-  __device__ void run_donated() {
+  // level-0 state of the branch donated to this worker; returns the R length
+  __device__ int prepare_donated(B& P, B& XP, int& nxx) {
     const Mailbox* mb = a.mbox + wid;
     const uint32_t* mbits = a.mbits + (size_t)wid * 2 * W;
     const int64_t r = mb->origin;
     const int rlen = mb->rlen;
-    const int nxx = mb->nxx;
-    B P, XP;
+    nxx = mb->nxx;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       P.w[k] = valid(k, lane) ? mbits[word(k)] : 0u;
       XP.w[k] = valid(k, lane) ? mbits[W + word(k)] : 0u;
     }
     adopt(mb, r);
-    traverse(P, XP, nxx, rlen, false);
+    return rlen;
   }
 };
 
@@ -1222,7 +1646,8 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem);
   uint32_t* s_p = reinterpret_cast<uint32_t*>(s_hist + HIST_SMEM);
-  uint32_t* s_rows = s_p + 3 * WARPS * SPW;
+  int32_t* s_cmp = reinterpret_cast<int32_t*>(s_p + 3 * WARPS * SPW);  // CMP_WORDS per warp
+  uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_cmp + WARPS * CMP_WORDS);
   int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? WARPS * W * CAPP : 0));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1232,21 +1657,33 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
   if (wid < a.num_workers) {
     Worker<W, PIVOT_XX, XROWS, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
                                   s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + 3 * warp * SPW,
-                                  s_hist);
+                                  s_hist, s_cmp + warp * CMP_WORDS);
     int stripe = wid % ROOT_STRIPES;
-    for (;;) {  // phase 1: claim independent subtrees (scheduler.py:253-273)
-      const int64_t idx = wk.claim_root(stripe);
-      if (idx < 0) break;
-      wk.roots_claimed++;
-      const long long t0 = a.root_cycles ? clock64() : 0;
-      wk.run_root(a.roots[idx]);
-      if (a.root_cycles && lane == 0) a.root_cycles[idx] = clock64() - t0;
-    }
-    if (a.worker_list_on) {  // phase 2: park, receive donated branches
-      while (wk.park()) {
+    bool phase1 = true;
+    // one traverse() call site (inlined once): phase 1 claims independent
+    // subtrees (scheduler.py:253-273), phase 2 parks on the worker list and
+    // receives donated branches
+    for (;;) {
+      Bits<W> P, XP;
+      int nxx = 0, rlen = 0;
+      int64_t idx = -1;
+      if (phase1) {
+        idx = wk.claim_root(stripe);
+        if (idx < 0) {
+          phase1 = false;
+          if (!a.worker_list_on) break;
+          continue;
+        }
+        wk.roots_claimed++;
+        rlen = wk.prepare_root(a.roots[idx], P, XP, nxx);
+      } else {
+        if (!wk.park()) break;
         wk.don_recv++;
-        wk.run_donated();
+        rlen = wk.prepare_donated(P, XP, nxx);
       }
+      const long long t0 = a.root_cycles ? clock64() : 0;
+      wk.traverse(P, XP, nxx, rlen, phase1);
+      if (phase1 && a.root_cycles && lane == 0) a.root_cycles[idx] = clock64() - t0;
     }
     if (lane == 0) {
       atomicAdd(&a.g_acc[0], wk.cliques);
@@ -1550,6 +1987,7 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
   constexpr int SPW = W < 32 ? 32 : W;
   size_t smem = HIST_SMEM * sizeof(unsigned int) + 3 * WARPS * SPW * sizeof(uint32_t) +
+                (size_t)WARPS * CMP_WORDS * sizeof(int32_t) +
                 (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
   if (g_tr) g_tr->mark("class start");
   int dev = 0, sms = 0;
@@ -1932,6 +2370,10 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.min_x = cfg->donation_min_x;
       args.heavy_rows = heavy_pool;
       args.heavy_off = hp.off;
+      {
+        const char* e = getenv("MCE_COMPACT");  // diagnostics: MCE_COMPACT=0 disables compact_run
+        args.compact = e ? atoi(e) : 1;
+      }
       {
         const char* e = getenv("MCE_XROWS_PARTIAL_MAX");  // diagnostics override
         args.xrows_partial_max = e ? atoi(e) : XROWS_PARTIAL_MAX;

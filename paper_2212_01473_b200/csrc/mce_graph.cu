@@ -486,6 +486,8 @@ constexpr int APEEL_THREADS = 256;
 #endif
 constexpr int APEEL_BATCH = MCE_APEEL_BATCH;  // queue slots a warp reserves at once
 constexpr unsigned long long TASK_EMPTY = ~0ull;
+constexpr int APEEL_TRACE_LEVELS = 4096;
+constexpr unsigned APEEL_MIN_PART = 256;
 
 struct APeelShared {
   alignas(128) unsigned int bar_count;
@@ -497,6 +499,9 @@ struct APeelShared {
   alignas(128) unsigned int acount;        // scan survivors
   int mindeg;
   unsigned int scan_claims;
+  int mindeg0;  // INT_MAX - minimum initial degree (max-reduced from the host's zero)
+  unsigned int part;              // warps consuming chunks in this level's async phase
+  unsigned long long head0;       // first queue slot of this level (static reservations)
 };
 
 template <typename F>
@@ -528,13 +533,15 @@ __device__ __forceinline__ void agrid_barrier(APeelShared* sh, unsigned int nblo
 template <int MAXC>
 __device__ __forceinline__ void apeel_claim(const int32_t (&cand)[MAXC], const int64_t (&e0)[MAXC],
                                             const int64_t (&e1)[MAXC],
-                                            int cnt, unsigned done, APeelShared* sh,
+                                            unsigned cmask, unsigned done, APeelShared* sh,
                                             uint64_t* __restrict__ tasks, int32_t* __restrict__ order,
                                             uint8_t* __restrict__ removed, int lane) {
+  // slot t holds a claim iff bit t of cmask (static indices: no local memory)
+  const int cnt = __popc(cmask);
   int nch = 0;
 #pragma unroll
   for (int t = 0; t < MAXC; ++t)
-    if (t < cnt) nch += (int)((e1[t] - e0[t] + 31) >> 5);
+    if ((cmask >> t) & 1u) nch += (int)((e1[t] - e0[t] + 31) >> 5);
   int ic = cnt, in = nch;  // inclusive warp scans of vertices and chunks
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -567,7 +574,7 @@ __device__ __forceinline__ void apeel_claim(const int32_t (&cand)[MAXC], const i
   unsigned long long tp = tpos + (unsigned)(in - nch);
 #pragma unroll
   for (int t = 0; t < MAXC; ++t) {
-    if (t < cnt) {
+    if ((cmask >> t) & 1u) {
       const int32_t v = cand[t];
       order[vp++] = v;
       removed[v] = 1;
@@ -586,56 +593,110 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
              int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
              uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
              int32_t* __restrict__ order, APeelShared* sh, int64_t* __restrict__ out_degeneracy,
-             unsigned poll_mask, unsigned sleep_ns) {
+             unsigned poll_mask, unsigned sleep_ns, unsigned long long* trace) {
   const unsigned int G = gridDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * APEEL_THREADS + threadIdx.x;
   const int64_t gstride = (int64_t)G * APEEL_THREADS;
   auto nothing = [] {};
+  int dmin = 0x7fffffff;
   for (int64_t v = gtid; v < n; v += gstride) {
-    deg[v] = (int32_t)(ro[v + 1] - ro[v]);
+    const int32_t d0 = (int32_t)(ro[v + 1] - ro[v]);
+    deg[v] = d0;
+    dmin = min(dmin, (int)d0);
     alive_a[v] = (int32_t)v;
     removed[v] = 0;
   }
+  // the first level is the minimum degree (no empty scans below it)
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0 && dmin != 0x7fffffff) atomicMax(&sh->mindeg0, 0x7fffffff - dmin);
   if (gtid == 0) sh->mindeg = 0x7fffffff;  // the rest of *sh is zeroed by the host
+  if (trace && gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace[8 * APEEL_TRACE_LEVELS]));
   agrid_barrier(sh, G, nothing);
   int32_t* alive = alive_a;
   int32_t* alive2 = alive_b;
   int64_t na = n;
-  int32_t k = 0, deg_max = 0;
+  int32_t k = 0x7fffffff - *(volatile int*)&sh->mindeg0, deg_max = 0;
   for (;;) {
-    // ---- scan: claim every live vertex with deg <= k (degrees are stable here)
-    for (int64_t base = gtid - lane; base < na; base += gstride) {
-      const int64_t i = base + lane;
-      int32_t v = -1, d = 0x7fffffff;
-      bool take = false, keep = false;
-      if (i < na) {
-        v = __ldcg(&alive[i]);
-        if (!__ldcg(&removed[v])) {
-          d = __ldcg(&deg[v]);
-          take = d <= k;
-          keep = !take;
-        }
+    // ---- scan: claim every live vertex with deg <= k (degrees are stable
+    // here).  A warp covers 32 * SCAN_U consecutive entries with every load
+    // issued before any is used (the scan is one dependent chain, not one
+    // per 32 entries), and makes one atomic per counter.
+    constexpr int SCAN_U = 8;
+    for (int64_t base = (gtid - lane) * SCAN_U; base < na; base += gstride * SCAN_U) {
+      int32_t v[SCAN_U], d[SCAN_U];
+      uint8_t rm[SCAN_U];
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        const int64_t i = base + u * 32 + lane;
+        v[u] = i < na ? __ldcg(&alive[i]) : -1;
       }
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      if (km) {
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        rm[u] = v[u] >= 0 ? __ldcg(&removed[v[u]]) : (uint8_t)1;
+        d[u] = v[u] >= 0 ? __ldcg(&deg[v[u]]) : 0x7fffffff;
+      }
+      int64_t e0[SCAN_U], e1[SCAN_U];
+      int nkeep = 0, md = 0x7fffffff;
+      unsigned km[SCAN_U], tmask = 0;
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        const bool live = !rm[u];
+        const bool take = live && d[u] <= k;
+        const bool keep = live && !take;
+        km[u] = __ballot_sync(0xffffffffu, keep);
+        nkeep += __popc(km[u]);
+        if (keep) md = min(md, (int)d[u]);
+        if (take) tmask |= 1u << u;
+      }
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        const bool t = (tmask >> u) & 1u;
+        e0[u] = t ? ro[v[u]] : 0;
+        e1[u] = t ? ro[v[u] + 1] : 0;
+      }
+      if (nkeep) {
         unsigned o = 0;
-        if (lane == 0) o = atomicAdd(&sh->acount, (unsigned)__popc(km));
+        if (lane == 0) o = atomicAdd(&sh->acount, (unsigned)nkeep);
         o = __shfl_sync(0xffffffffu, o, 0);
-        if (keep) alive2[o + __popc(km & ((1u << lane) - 1))] = v;
-        const int md = __reduce_min_sync(0xffffffffu, keep ? d : 0x7fffffff);
+        const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+        for (int u = 0; u < SCAN_U; ++u) {
+          if ((km[u] >> lane) & 1u) alive2[o + __popc(km[u] & lt)] = v[u];
+          o += __popc(km[u]);
+        }
+        md = __reduce_min_sync(0xffffffffu, md);
         if (lane == 0) atomicMin(&sh->mindeg, md);
       }
-      const unsigned tm = __ballot_sync(0xffffffffu, take);
-      if (tm) {
-        if (lane == 0) atomicAdd(&sh->scan_claims, (unsigned)__popc(tm));
-        int32_t c1[1] = {v};
-        int64_t a1[1] = {take ? ro[v] : 0}, b1[1] = {take ? ro[v + 1] : 0};
-        apeel_claim<1>(c1, a1, b1, take ? 1 : 0, 0u, sh, tasks, order, removed, lane);
+      const int ntake = __reduce_add_sync(0xffffffffu, __popc(tmask));
+      if (ntake) {
+        if (lane == 0) atomicAdd(&sh->scan_claims, (unsigned)ntake);
+        apeel_claim<SCAN_U>(v, e0, e1, tmask, 0u, sh, tasks, order, removed, lane);
       }
     }
-    agrid_barrier(sh, G, nothing);
+    // the async phase's consumers: about one warp per 4 queued chunks (at
+    // least APEEL_MIN_PART), each starting on its own statically assigned
+    // reservation -- a small level does not send every warp of the grid
+    // through one contended head counter
+    const unsigned total_warps = G * (APEEL_THREADS / 32);
+    agrid_barrier(sh, G, [sh, total_warps] {
+      const unsigned long long h0 = sh->head;
+      const unsigned long long t0 = sh->tclaim;
+      unsigned long long part = (t0 - h0 + 3) / 4;
+      part = part < APEEL_MIN_PART ? APEEL_MIN_PART : part;
+      part = part > total_warps ? total_warps : part;
+      sh->part = (unsigned)part;
+      sh->head0 = h0;
+      sh->head = h0 + part * APEEL_BATCH;
+    });
     const unsigned claims = *(volatile unsigned*)&sh->scan_claims;
+    if (trace && gtid == 0 && k < APEEL_TRACE_LEVELS) {  // diagnostics (MCE_PEEL_TRACE)
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[8 * k + 0] = t;
+      trace[8 * k + 1] = claims;
+      trace[8 * k + 2] = na;
+    }
     const unsigned vc = *(volatile unsigned*)&sh->vclaim;
     const int32_t mn = *(volatile int*)&sh->mindeg;
     na = *(volatile unsigned*)&sh->acount;
@@ -649,6 +710,7 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
     if (claims == 0) {
       k = max(k + 1, mn);
       agrid_barrier(sh, G, [sh] {
+        sh->head = sh->tclaim;  // undo the (empty) level's static reservations
         sh->acount = 0;
         sh->mindeg = 0x7fffffff;
       });
@@ -656,11 +718,18 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
     }
     // ---- asynchronous phase: consume chunks until quiescence
     const int32_t kp1 = k + 1;
-    bool over = false;
+    const unsigned gw = (unsigned)(gtid >> 5);
+    bool over = gw >= *(volatile unsigned*)&sh->part;
+    bool first = true;
     while (!over) {
       unsigned long long h = 0;
-      if (lane == 0) h = atomicAdd(&sh->head, (unsigned long long)APEEL_BATCH);
-      h = __shfl_sync(0xffffffffu, h, 0);
+      if (first) {
+        h = *(volatile unsigned long long*)&sh->head0 + (unsigned long long)gw * APEEL_BATCH;
+        first = false;
+      } else {
+        if (lane == 0) h = atomicAdd(&sh->head, (unsigned long long)APEEL_BATCH);
+        h = __shfl_sync(0xffffffffu, h, 0);
+      }
       int got = 0;
       while (got < APEEL_BATCH) {
         uint64_t dsc = TASK_EMPTY;
@@ -677,6 +746,12 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
             const unsigned long long cl = __ldcv(&sh->tclaim);
             if ((cl == dn && h + got >= cl) || __ldcv(&sh->vclaim) >= (unsigned)n) {
               over = true;
+              if (trace && lane == 0 && k < APEEL_TRACE_LEVELS) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                atomicMin(&trace[8 * k + 4], t);
+                atomicMax(&trace[8 * k + 5], t);
+              }
               break;
             }
           }
@@ -684,9 +759,6 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
         }
         if (over) break;
         // c chunks: lane l takes edge l of each; c decrements in flight per lane
-        int32_t cand[APEEL_BATCH];
-        int64_t c0[APEEL_BATCH], c1[APEEL_BATCH];
-        int cnt = 0;
         int32_t u[APEEL_BATCH];
 #pragma unroll
         for (int t = 0; t < APEEL_BATCH; ++t) {
@@ -704,17 +776,18 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
           r1[t] = u[t] >= 0 ? __ldg(&ro[u[t] + 1]) : 0;
           old_deg[t] = u[t] >= 0 ? atomicSub(&deg[u[t]], 1) : 0;
         }
+        unsigned cm = 0;
 #pragma unroll
-        for (int t = 0; t < APEEL_BATCH; ++t) {
-          if (u[t] >= 0 && old_deg[t] == kp1) {
-            cand[cnt] = u[t];
-            c0[cnt] = r0[t];
-            c1[cnt] = r1[t];
-            ++cnt;
-          }
-        }
-        apeel_claim<APEEL_BATCH>(cand, c0, c1, cnt, (unsigned)c, sh, tasks, order, removed, lane);
+        for (int t = 0; t < APEEL_BATCH; ++t)
+          if (u[t] >= 0 && old_deg[t] == kp1) cm |= 1u << t;
+        apeel_claim<APEEL_BATCH>(u, r0, r1, cm, (unsigned)c, sh, tasks, order, removed, lane);
         got += c;
+        if (trace && lane == 0 && k < APEEL_TRACE_LEVELS) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          atomicMax(&trace[8 * k + 6], t);
+          atomicAdd(&trace[8 * k + 7], (unsigned long long)c);
+        }
       }
     }
     // the next scan runs on quiescent degrees; consumers restart at the queue end
@@ -724,6 +797,11 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
       sh->acount = 0;
       sh->mindeg = 0x7fffffff;
     });
+    if (trace && gtid == 0 && k < APEEL_TRACE_LEVELS) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[8 * k + 3] = t;
+    }
     k += 1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
@@ -1086,12 +1164,41 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
   MCE_CHECK(cudaMemsetAsync(tasks, 0xff, sizeof(uint64_t) * task_cap, s));
   MCE_CHECK(cudaMemsetAsync(sh, 0, sizeof(APeelShared), s));  // mindeg: set by the kernel
   mce_trace_mark("peel setup");
+  // diagnostics: MCE_PEEL_TRACE=<file> writes per level (k, scan end ns, scan claims,
+  // alive scanned, level end ns) relative to the kernel start
+  const char* trace_path = getenv("MCE_PEEL_TRACE");
+  unsigned long long* trace = nullptr;
+  const size_t trace_words = 8 * APEEL_TRACE_LEVELS + 1;
+  if (trace_path) {
+    if (scr.get(&trace, trace_words)) return -1;
+    MCE_CHECK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * trace_words, s));
+    for (int k = 0; k < APEEL_TRACE_LEVELS; ++k)  // first-quiescence slots start at ~0 (atomicMin)
+      MCE_CHECK(cudaMemsetAsync(trace + 8 * k + 4, 0xff, sizeof(unsigned long long), s));
+  }
   k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                    removed, order, sh, d_degeneracy,
                                                    apeel_env("MCE_APEEL_POLL", 3),
-                                                   apeel_env("MCE_APEEL_SLEEP", 32));
+                                                   apeel_env("MCE_APEEL_SLEEP", 32), trace);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
+  if (trace) {
+    std::vector<unsigned long long> h(trace_words);
+    MCE_CHECK(cudaMemcpyAsync(h.data(), trace, sizeof(unsigned long long) * trace_words,
+                              cudaMemcpyDeviceToHost, s));
+    MCE_CHECK(cudaStreamSynchronize(s));
+    if (FILE* f = fopen(trace_path, "a")) {
+      const unsigned long long t0 = h[8 * APEEL_TRACE_LEVELS];
+      auto us = [&](unsigned long long t) { return (t && t != ~0ull) ? (double)(t - t0) / 1e3 : -1.0; };
+      fprintf(f, "# n=%lld grid=%lld: k scan_end_us claims alive first_quiesce_us last_quiesce_us "
+                 "last_work_us chunks level_end_us\n", (long long)n, (long long)grid);
+      for (int k = 0; k < APEEL_TRACE_LEVELS; ++k)
+        if (h[8 * k])
+          fprintf(f, "%d %.1f %llu %llu %.1f %.1f %.1f %llu %.1f\n", k, us(h[8 * k]), h[8 * k + 1],
+                  h[8 * k + 2], us(h[8 * k + 4]), us(h[8 * k + 5]), us(h[8 * k + 6]), h[8 * k + 7],
+                  us(h[8 * k + 3]));
+      fclose(f);
+    }
+  }
   k_peel_positions<<<grid_for(n), 256, 0, s>>>(order, n, d_pos);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());

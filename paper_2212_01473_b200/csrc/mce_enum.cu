@@ -49,6 +49,9 @@
 
 namespace {
 
+#ifndef MCE_CMP_NARROW_MAX_W
+#define MCE_CMP_NARROW_MAX_W 1
+#endif
 constexpr int HIST_SMEM = 128;
 constexpr int CMP_WORDS = 256;  // per-warp compact_run scratch: 64 + 64 ints, 64 x 8-byte rows
 constexpr int HIST_MAX = MCE_HIST_MAX;
@@ -101,6 +104,7 @@ struct EnumArgs {
   const uint64_t* vhash;  // mix64(label(v))
   const int64_t* roots;   // l1: vertex, l2: (u << 32) | v
   int64_t num_roots;
+  const unsigned long long* num_roots_dev;  // if set: the root count, written by an earlier kernel
   unsigned long long* root_counter;  // ROOT_STRIPES counters, ROOT_STRIDE apart
   int roots_mode;
   int num_workers;
@@ -220,6 +224,9 @@ struct Worker {
   static constexpr int CAPP = CAP + 1;
   static constexpr int K = (W + 31) / 32;
   static constexpr int SPW = W < 32 ? 32 : W;
+  // the register-starved narrow classes instantiate only the 32-slot compact
+  // copy (|P| <= 32 there anyway; a 64-slot copy would only serve > 32 live X_X)
+  static constexpr bool CMP_NARROW_ONLY = W <= MCE_CMP_NARROW_MAX_W;
   using B = Bits<W>;
 
   const EnumArgs& a;
@@ -259,6 +266,7 @@ struct Worker {
   long long nodes = 0, roots_claimed = 0, don_made = 0, don_recv = 0;
   unsigned long long cliques = 0, hash = 0, max_size = 0;
   bool phase2_seen = false;
+  int64_t nroots = 0;  // a.num_roots, or the count an earlier kernel left in a.num_roots_dev
 
   __device__ Worker(const EnumArgs& args, int lane_, int wid_, uint32_t* smem_rows,
                     int32_t* smem_plist, uint32_t* smem_p, unsigned int* smem_hist,
@@ -273,6 +281,7 @@ struct Worker {
       rowsT = a.rows_g + (size_t)wid * W * CAPP;
       plist = a.plist_g + (size_t)wid * CAP;
     }
+    nroots = a.num_roots_dev ? (int64_t)*(volatile const unsigned long long*)a.num_roots_dev : a.num_roots;
     xrows_own = XROWS ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
     xrowsT = xrows_own;
     xstride = a.xcap;
@@ -729,8 +738,8 @@ struct Worker {
         bool leaf = false, xclear = false;
         if (cand) {
           uint32_t pin = 0, xin = 0;
-#pragma unroll
           constexpr int RB = W >= 8 ? 4 : 1;  // row words in flight (see count_in_p)
+#pragma unroll
           for (int q = 0; q < K; ++q) {
             for (unsigned um = umask[q]; um;) {
               int jj[RB];
@@ -825,7 +834,7 @@ struct Worker {
       const unsigned long long c =
           lane < ROOT_STRIPES ? *(volatile unsigned long long*)&a.root_counter[lane * ROOT_STRIDE] : 0ull;
       const bool done = lane >= ROOT_STRIPES ||
-                        c * ROOT_STRIPES + lane >= (unsigned long long)a.num_roots;
+                        c * ROOT_STRIPES + lane >= (unsigned long long)nroots;
       phase2_seen = __all_sync(FULLMASK, done);
     }
     return phase2_seen;
@@ -841,7 +850,7 @@ struct Worker {
       if (lane == 0) idx = atomicAdd(&a.root_counter[stripe * ROOT_STRIDE], 1ull);
       idx = __shfl_sync(FULLMASK, idx, 0);
       const unsigned long long r = idx * ROOT_STRIPES + stripe;
-      if (r < (unsigned long long)a.num_roots) return (int64_t)r;
+      if (r < (unsigned long long)nroots) return (int64_t)r;
       stripe = (stripe + 1) % ROOT_STRIPES;
     }
     return -1;
@@ -1021,6 +1030,7 @@ struct Worker {
     for (int k = 0; k < K; ++k) c += __popc(P.w[k] | XP.w[k]);
     c = __reduce_add_sync(FULLMASK, c);
     if (c > 64) return 0;
+    if (CMP_NARROW_ONLY) return (c <= 32 && live <= 32) ? 32 : 0;
     return (c <= 32 && live <= 32) ? 32 : 64;
   }
 
@@ -1422,7 +1432,7 @@ struct Worker {
         const int cw = compact_width(P, XP, live);
         if (cw) {  // the whole subtree below this node, on the register copy
           const uint64_t hs0 = hsum[rlen];
-          if (cw == 32) compact_run<uint32_t>(P, XP, live, rlen, below, hs0);
+          if (cw == 32 || CMP_NARROW_ONLY) compact_run<uint32_t>(P, XP, live, rlen, below, hs0);
           else compact_run<unsigned long long>(P, XP, live, rlen, below, hs0);
 #pragma unroll
           for (int k = 0; k < K; ++k) NL.w[k] = 0;
@@ -1702,6 +1712,8 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
   for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&a.g_hist[i], (unsigned long long)s_hist[i]);
 }
+
+#include "mce_tiny.cuh"
 
 // ------------------------------------------------------------ root prep
 
@@ -2096,6 +2108,42 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
   return -3;
 }
 
+// the lane-per-root kernel over the |P| <= 32 roots, timed by its own event pair
+int launch_tiny(bool full, TinyArgs ta, cudaStream_t s, cudaEvent_t* ev, int64_t* launches,
+                int64_t* workers_used) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  static int per_sm[2][64];
+  static bool have[2][64];
+  const size_t smem = sizeof(uint32_t) * TINY_SMEM_WORDS;
+  auto kern = full ? k_tiny<true> : k_tiny<false>;
+  if (!have[full][dev]) {
+    MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[full][dev], kern, TINY_THREADS, smem));
+    have[full][dev] = true;
+  }
+  if (per_sm[full][dev] < 1) {
+    mce_set_error("tiny-root kernel does not fit on an SM");
+    return -3;
+  }
+  // one warp claims 32 roots: no more CTAs than that keeps busy
+  const int64_t need = (ta.num_roots + TINY_THREADS - 1) / TINY_THREADS;
+  int64_t g = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm[full][dev] * sms, need));
+  if (ta.max_warps > 0) g = std::min<int64_t>(g, (ta.max_warps + TINY_WARPS - 1) / TINY_WARPS);
+  else ta.max_warps = (int)(g * TINY_WARPS);
+  const int grid = (int)g;
+  *workers_used = std::max<int64_t>(*workers_used, ta.max_warps);
+  MCE_CHECK(cudaEventRecord(ev[0], s));
+  kern<<<grid, TINY_THREADS, smem, s>>>(ta);
+  mce_count_launch();
+  MCE_CHECK(cudaEventRecord(ev[1], s));
+  MCE_CHECK(cudaGetLastError());
+  (*launches)++;
+  return 0;
+}
+
 // Partial mode ("ip") keeps the reference's pivot rule (P | X_P only) but, when
 // HBM allows, still materialises the X rows so X_X adjacency is one bit test
 // instead of a binary search of the CSR -- same traversal tree, fewer
@@ -2212,7 +2260,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   int64_t workers_used = 0;
   // timing events, created once per device (one call at a time uses them: the
   // call holds them until its final synchronisation)
-  static cudaEvent_t ev_cache[64][2 * NUM_WIDTHS];
+  static cudaEvent_t ev_cache[64][2 * (NUM_WIDTHS + 1)];
   static bool ev_have[64];
   static std::mutex ev_mu;
   std::unique_lock<std::mutex> ev_lock(ev_mu);
@@ -2220,7 +2268,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   cudaGetDevice(&ev_dev);
   if (ev_dev < 0 || ev_dev >= 64) ev_dev = 0;
   if (!ev_have[ev_dev]) {
-    for (int e = 0; e < 2 * NUM_WIDTHS; ++e) MCE_CHECK(cudaEventCreate(&ev_cache[ev_dev][e]));
+    for (int e = 0; e < 2 * (NUM_WIDTHS + 1); ++e) MCE_CHECK(cudaEventCreate(&ev_cache[ev_dev][e]));
     ev_have[ev_dev] = true;
   }
   cudaEvent_t* events = ev_cache[ev_dev];
@@ -2246,6 +2294,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     unsigned long long* cls = zb + ZB_CLS;  // zeroed above
     constexpr int HMETA = MAXP_SLOT + 1;  // cls[HMETA .. HMETA+2] = heavy plan counters
     static_assert(HMETA + 3 <= 16, "class/heavy counters exceed their zeroed slots");
+    constexpr int TINY_SLOT = HMETA + 3;  // k_tiny's claim counter and fallback length
+    static_assert(TINY_SLOT + 2 <= 16, "tiny counters exceed their zeroed slots");
     if (get(&keys, count) || get(&keys2, count) || get(&roots, count) || get(&roots2, count)) {
       cleanup();
       return -1;
@@ -2377,6 +2427,41 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       {
         const char* e = getenv("MCE_XROWS_PARTIAL_MAX");  // diagnostics override
         args.xrows_partial_max = e ? atoi(e) : XROWS_PARTIAL_MAX;
+      }
+      // |P| <= 32: one root per lane (k_tiny); the roots it hands back (heavy X,
+      // dense, many X_X rows) follow in the warp kernel, whose root count the
+      // device supplies
+      // diagnostics: MCE_TINY=<min class size> (0 disables the lane-per-root path)
+      const char* te = getenv("MCE_TINY");
+      // (a small class is latency-bound either way: one warp kernel, one launch)
+      const int64_t tiny_min = te ? std::max(0, atoi(te)) : TINY_MIN_ROOTS;
+      if (cp.W == 1 && cfg->roots == 1 && cfg->collect_cap <= 0 && tiny_min > 0 && cp.count >= tiny_min) {
+        int64_t* fb = nullptr;
+        if (get(&fb, cp.count)) {
+          cleanup();
+          return -1;
+        }
+        TinyArgs ta{};
+        ta.ro = g->ro;
+        ta.col = g->col;
+        ta.split = g->split;
+        ta.vhash = vhash;
+        ta.roots = sorted_roots + cp.begin;
+        ta.num_roots = cp.count;
+        ta.counter = cls + TINY_SLOT;
+        ta.fallback = fb;
+        ta.fallback_len = cls + TINY_SLOT + 1;
+        ta.g_acc = acc;
+        ta.g_hist = hist;
+        ta.w_metrics = wmet;
+        ta.phase_ns = nullptr;
+        ta.max_warps = cfg->workers > 0 ? cfg->workers : 0;
+        if (launch_tiny(full, ta, s, &events[2 * nev++], &launches, &workers_used)) {
+          cleanup();
+          return -1;
+        }
+        args.roots = fb;
+        args.num_roots_dev = cls + TINY_SLOT + 1;
       }
       int req = cfg->workers > 0 ? cfg->workers : 0;
       if (req <= 0) req = 0;

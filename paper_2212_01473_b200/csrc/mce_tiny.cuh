@@ -1,0 +1,407 @@
+// Thread-per-root enumeration of the tiny first-level roots (|P| <= 32): the
+// narrowest subwarp partition -- a bitset over the root's P is ONE 32-bit
+// register, so each lane of a warp runs a whole root on its own and a warp
+// works 32 roots at once (the warp-per-root Worker leaves most lanes idle on
+// a 10-member P).  Included by mce_enum.cu inside its anonymous namespace.
+//
+// Same traversal as Worker::traverse / compact_run (reference bk.py:82-110,
+// scheduler.py:297-381, xsets.py:55-82): pivot = max |N(c) & P| over
+// P | X_P, ties to the smallest id, full mode's X_X rows only when strictly
+// better (first in prefix order); leaves of a node settled in one pass; the
+// X_X prefix stably partitioned in place on descent and never restored -- so
+// node totals are identical to the warp kernels'.
+//
+// A warp claims 32 consecutive roots of the (heaviest-first) class list and
+//  * builds them TOGETHER: the N+ lists of all their P and X members are one
+//    flattened stream over the lanes (coalesced loads, 128 in flight per
+//    warp, the same walk as Worker::build), hits OR-ed into each root's rows
+//    in shared memory -- a lane walking its own root's lists alone would
+//    issue 32 uncoalesced sectors per load instruction;
+//  * then runs one root per lane: member list, induced rows and X rows of
+//    root r at [r * 33 + i] of the warp's shared-memory slices (33: distinct
+//    banks across lanes), the DFS frames in local memory (L1).
+//
+// A root leaves this path for the warp kernel (appended to `fallback`) when
+// it has a heavy-X pool slot, more than TINY_XT earlier neighbours, or more
+// than TINY_E_MAX induced edges (a bound on its subtree: one lane must not
+// carry a big search tree).
+
+constexpr int TINY_WARPS = 8;
+constexpr int64_t TINY_MIN_ROOTS = 8192;  // smaller W = 1 classes stay on the warp kernel
+constexpr int TINY_THREADS = 32 * TINY_WARPS;
+constexpr int TINY_XT = 32;    // X members per root (|X| <= 32)
+constexpr int TINY_STRIDE = 33;
+constexpr int TINY_SLICE = 32 * TINY_STRIDE;  // words per warp per array
+#ifndef MCE_TINY_E_MAX
+#define MCE_TINY_E_MAX 64
+#endif
+constexpr int TINY_E_MAX = MCE_TINY_E_MAX;
+// a clique of c members in P needs c(c-1)/2 <= TINY_E_MAX edges
+constexpr int tiny_max_clique(int e) {
+  int c = 1;
+  while ((c + 1) * c / 2 <= e) ++c;
+  return c;
+}
+constexpr int TINY_DEPTH = tiny_max_clique(TINY_E_MAX) + 1;
+constexpr int TINY_SMEM_WORDS = HIST_SMEM + 3 * TINY_SLICE * TINY_WARPS;
+
+struct TinyArgs {
+  const int64_t* ro;
+  const int32_t* col;
+  const int64_t* split;
+  const uint64_t* vhash;
+  const int64_t* roots;
+  int64_t num_roots;
+  unsigned long long* counter;       // roots claimed (batches of 32, one per warp)
+  int64_t* fallback;                 // roots handed to the warp kernel
+  unsigned long long* fallback_len;
+  unsigned long long* g_acc;         // 0 cliques, 1 hash, 2 nodes, 3 donations, 4 max size
+  unsigned long long* g_hist;
+  long long* w_metrics;              // per warp: nodes, roots, donations made, received
+  unsigned long long* phase_ns;      // [0] first start (min), [1] phase-2 start (min), [2] end (max)
+  int max_warps;                     // workers requested (warps >= this stay idle)
+};
+
+__device__ __forceinline__ void tiny_hist_add(unsigned* s_hist, unsigned long long* g_hist, int size) {
+  const unsigned old = atomicAdd(&s_hist[size], 1u);
+  if (old == 0x7fffffffu) {  // spill 2^31 to HBM
+    atomicAdd(&g_hist[size], 0x80000000ull);
+    atomicSub(&s_hist[size], 0x80000000u);
+  }
+}
+
+// index of w in the padded 32-entry member list pl (5 branchless steps), -1 if absent
+__device__ __forceinline__ int tiny_find(const int32_t* pl, int32_t w) {
+  int i = 0;
+  i += pl[i + 15] < w ? 16 : 0;
+  i += pl[i + 7] < w ? 8 : 0;
+  i += pl[i + 3] < w ? 4 : 0;
+  i += pl[i + 1] < w ? 2 : 0;
+  i += pl[i] < w ? 1 : 0;
+  return pl[i] == w ? i : -1;
+}
+
+// The lane's root r = lane: DFS over its rows (same rules as compact_run).
+template <bool PIVOT_XX>
+__device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, const uint32_t* rows,
+                                         uint32_t* xm, int np, int live, uint64_t hs,
+                                         unsigned* s_hist, unsigned long long& cliques,
+                                         unsigned long long& hash, unsigned long long& nodes,
+                                         unsigned long long& max_size) {
+  uint32_t P = np == 32 ? ~0u : ((1u << np) - 1u), XP = 0, BR = 0, NL = 0;
+  int rlen = 1, depth = 0;
+  nodes++;
+  // depth <= (max clique size in P) - 1 <= TINY_DEPTH - 1 under TINY_E_MAX edges
+  uint32_t fP[TINY_DEPTH], fXP[TINY_DEPTH], fBR[TINY_DEPTH], fNL[TINY_DEPTH];
+  int flive[TINY_DEPTH];
+  uint64_t fhs[TINY_DEPTH];
+  bool fresh = true;
+  for (;;) {
+    if (fresh) {
+      fresh = false;
+      // pivot (bk.py:82-110): max |N(c) & P| over P | X_P, ties to the smallest id
+      int best = -1;
+      uint32_t prow = 0;
+      for (uint32_t t = P | XP; t; t &= t - 1) {
+        const uint32_t r = rows[__ffs(t) - 1];
+        const int c = __popc(r & P);
+        if (c > best) {
+          best = c;
+          prow = r;
+        }
+      }
+      uint32_t xxadj = 0;
+      for (int i = 0; i < live; ++i) {
+        const uint32_t r = xm[i];
+        xxadj |= r;
+        if (PIVOT_XX) {  // X_X rows win only when strictly better, first in prefix order
+          const int c = __popc(r & P);
+          if (c > best) {
+            best = c;
+            prow = r;
+          }
+        }
+      }
+      BR = P & ~prow;
+      // leaf batch: every branch whose child P is empty (see Worker::leaf_batch)
+      const int size = rlen + 1;
+      uint32_t leafm = 0;
+      for (uint32_t t = BR; t; t &= t - 1) {
+        const int sl = __ffs(t) - 1;
+        const uint32_t bit = 1u << sl;
+        const uint32_t before = BR & (bit - 1u);
+        const uint32_t r = rows[sl];
+        if ((r & (P & ~before)) == 0) {
+          leafm |= bit;
+          if ((r & (XP | before)) == 0 && !(xxadj & bit)) {
+            cliques++;
+            hash += mce_mix64(hs + __ldg(&a.vhash[pl[sl]]) + (uint64_t)size * MCE_SIZE_SALT);
+            if ((unsigned long long)size > max_size) max_size = size;
+            tiny_hist_add(s_hist, a.g_hist, size);
+          }
+        }
+      }
+      nodes += __popc(leafm);
+      NL = BR & ~leafm;
+    }
+    if (NL == 0) {
+      if (depth == 0) break;
+      depth--;
+      rlen--;
+      P = fP[depth];
+      XP = fXP[depth];
+      BR = fBR[depth];
+      NL = fNL[depth];
+      live = flive[depth];
+      hs = fhs[depth];
+      continue;
+    }
+    // move v and the (leaf) branches before it from P to X_P
+    const int vs = __ffs(NL) - 1;
+    const uint32_t bit = 1u << vs;
+    const uint32_t mv = (BR & (bit - 1u)) | bit;
+    BR &= ~mv;
+    NL &= ~mv;
+    P &= ~mv;
+    XP |= mv;
+    const uint32_t rv = rows[vs];
+    // stable partition of the live X_X prefix by adjacency to v (xsets.py:55-82);
+    // the parent's prefix stays permuted (the reference never restores it)
+    // (in place: a kept row moves down over the dropped block, which shifts up)
+    int kept = 0;
+    for (int i = 0; i < live; ++i) {
+      const uint32_t r = xm[i];
+      if ((r >> vs) & 1u) {
+        for (int j = i; j > kept; --j) xm[j] = xm[j - 1];
+        xm[kept++] = r;
+      }
+    }
+    fP[depth] = P;
+    fXP[depth] = XP;
+    fBR[depth] = BR;
+    fNL[depth] = NL;
+    flive[depth] = live;
+    fhs[depth] = hs;
+    depth++;
+    live = kept;
+    XP &= rv;
+    P &= rv;
+    hs += __ldg(&a.vhash[pl[vs]]);
+    rlen++;
+    nodes++;
+    fresh = true;
+  }
+}
+
+template <bool PIVOT_XX>
+__global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
+  extern __shared__ __align__(16) uint32_t tsm[];
+  unsigned* s_hist = tsm;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  int32_t* spl = reinterpret_cast<int32_t*>(tsm + HIST_SMEM) + warp * 3 * TINY_SLICE;
+  uint32_t* srow = reinterpret_cast<uint32_t*>(spl + TINY_SLICE);
+  uint32_t* sxb = srow + TINY_SLICE;
+  for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  const int gw = (int)((blockIdx.x * TINY_THREADS + threadIdx.x) >> 5);
+  const int32_t* __restrict__ col = a.col;
+  if (a.phase_ns && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&a.phase_ns[0], t);
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long cliques = 0, hash = 0, nodes = 0, max_size = 0;
+  long long claimed = 0;
+  int32_t* mypl = spl + lane * TINY_STRIDE;
+  uint32_t* myrow = srow + lane * TINY_STRIDE;
+  uint32_t* myxb = sxb + lane * TINY_STRIDE;
+  for (;;) {
+    if (gw >= a.max_warps) break;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.counter, 32ull);
+    base = __shfl_sync(FULLMASK, base, 0);
+    if (base >= (unsigned long long)a.num_roots) break;
+    // ---- lane r: root r of the batch
+    const int64_t idx = (int64_t)base + lane;
+    const bool valid = idx < a.num_roots;
+    const int64_t renc = valid ? a.roots[idx] : 0;
+    const int64_t v = renc & ROOT_ID_MASK;
+    int64_t xb0 = 0, s0 = 0;
+    int np = 0, nx = 0;
+    if (valid) {
+      xb0 = a.ro[v];
+      s0 = a.split[v];
+      np = (int)(a.ro[v + 1] - s0);
+      nx = (int)(s0 - xb0);
+    }
+    bool ok = valid && (renc >> ROOT_ID_BITS) == 0 && np <= 32 && nx <= TINY_XT;
+    if (!ok) np = nx = 0;
+    // member list (padded for tiny_find), zeroed rows
+    for (int k = 0; k < 32; ++k) mypl[k] = 0x7fffffff;
+    for (int k = 0; k < np; ++k) myrow[k] = 0;
+    for (int t = 0; t < nx; ++t) myxb[t] = 0;
+    __syncwarp();  // other lanes fill this root's member list below
+    // ---- build, all 32 roots at once.  Member q of the batch: root r's P
+    // members first (np_r), then its X members (nx_r).
+    const int cnt = np + nx;
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(FULLMASK, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(FULLMASK, incl, 31);
+    // P member lists: one coalesced pass over the roots' N+ ranges
+    for (int q0 = 0; q0 < total; q0 += 32) {
+      const int q = q0 + lane;
+      int r = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int ic = __shfl_sync(FULLMASK, incl, r + step - 1);
+        if (ic <= q) r += step;
+      }
+      const int k = q - __shfl_sync(FULLMASK, excl, r);
+      const int npr = __shfl_sync(FULLMASK, np, r);
+      const int64_t sr = __shfl_sync(FULLMASK, s0, r);
+      if (q < total && k < npr) spl[r * TINY_STRIDE + k] = __ldg(&col[sr + k]);
+    }
+    __syncwarp();
+    for (int q0 = 0; q0 < total; q0 += 32) {
+      // lane: member q0 + lane -> its root, kind, index and N+ range
+      const int q = q0 + lane;
+      int r = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int ic = __shfl_sync(FULLMASK, incl, r + step - 1);
+        if (ic <= q) r += step;
+      }
+      const int k = q - __shfl_sync(FULLMASK, excl, r);
+      const int npr = __shfl_sync(FULLMASK, np, r);
+      const int64_t xr = __shfl_sync(FULLMASK, xb0, r);
+      int64_t lo = 0;
+      int len = 0;
+      int info = 0;  // root (5 bits) | X member (bit 5) | index (bits 6..)
+      if (q < total) {
+        int32_t m;
+        if (k < npr) {
+          m = spl[r * TINY_STRIDE + k];
+          info = r | (k << 6);
+        } else {
+          m = __ldg(&col[xr + (k - npr)]);
+          info = r | 32 | ((k - npr) << 6);
+        }
+        lo = __ldg(&a.split[m]);
+        len = (int)(__ldg(&a.ro[m + 1]) - lo);
+      }
+      // flatten the 32 members' N+ lists over the lanes (see warp_flat_walk)
+      int inc2 = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, inc2, d);
+        if (lane >= d) inc2 += t;
+      }
+      const int exc2 = inc2 - len;
+      const int tot2 = __shfl_sync(FULLMASK, inc2, 31);
+      constexpr int U = 4;
+      for (int b2 = 0; b2 < tot2; b2 += 32 * U) {
+        int32_t val[U];
+        int inf[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int kk = b2 + u * 32 + lane;
+          int o = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int ic = __shfl_sync(FULLMASK, inc2, o + step - 1);
+            if (ic <= kk) o += step;
+          }
+          const int64_t lo_o = __shfl_sync(FULLMASK, lo, o);
+          const int ex_o = __shfl_sync(FULLMASK, exc2, o);
+          inf[u] = __shfl_sync(FULLMASK, info, o);
+          val[u] = kk < tot2 ? __ldg(&col[lo_o + (kk - ex_o)]) : 0x7fffffff;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (b2 + u * 32 + lane < tot2) {
+            const int rr = inf[u] & 31;
+            const int j = tiny_find(spl + rr * TINY_STRIDE, val[u]);
+            if (j >= 0) {
+              const int ii = inf[u] >> 6;
+              if (inf[u] & 32) {
+                atomicOr(&sxb[rr * TINY_STRIDE + ii], 1u << j);
+              } else {  // N+(p_ii) holds only members after ii
+                atomicOr(&srow[rr * TINY_STRIDE + ii], 1u << j);
+                atomicOr(&srow[rr * TINY_STRIDE + j], 1u << ii);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // ---- lane r enumerates root r
+    if (ok) {
+      int e2 = 0;
+      for (int k = 0; k < np; ++k) e2 += __popc(myrow[k]);
+      if (e2 > 2 * TINY_E_MAX) {
+        ok = false;
+      } else {
+        // X members with no neighbour in P never matter (see init_tokens)
+        int nxx = 0;
+        for (int t = 0; t < nx; ++t) {
+          const uint32_t mk = myxb[t];
+          if (mk) myxb[nxx++] = mk;
+        }
+        if (np > 0) {
+          tiny_dfs<PIVOT_XX>(a, mypl, myrow, myxb, np, nxx, __ldg(&a.vhash[v]), s_hist, cliques,
+                             hash, nodes, max_size);
+          claimed++;
+        }
+      }
+    }
+    const bool fb = valid && !ok;
+    const unsigned fm = __ballot_sync(FULLMASK, fb);
+    if (fm) {
+      unsigned long long o = 0;
+      if (lane == 0) o = atomicAdd(a.fallback_len, (unsigned long long)__popc(fm));
+      o = __shfl_sync(FULLMASK, o, 0);
+      if (fb) a.fallback[o + __popc(fm & lt)] = renc;
+    }
+    __syncwarp();
+  }
+  if (a.phase_ns && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&a.phase_ns[1], t);  // this warp found the root list exhausted
+    atomicMax(&a.phase_ns[2], t);
+  }
+  // warp totals (64-bit shuffles), one set of atomics per warp
+  unsigned long long c = cliques, h = hash, nd = nodes, mx = max_size;
+  long long rc = claimed;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(FULLMASK, c, o);
+    h += __shfl_xor_sync(FULLMASK, h, o);
+    nd += __shfl_xor_sync(FULLMASK, nd, o);
+    rc += __shfl_xor_sync(FULLMASK, rc, o);
+    const unsigned long long m2 = __shfl_xor_sync(FULLMASK, mx, o);
+    mx = m2 > mx ? m2 : mx;
+  }
+  if (lane == 0 && gw < a.max_warps) {
+    if (c) {
+      atomicAdd(&a.g_acc[0], c);
+      atomicAdd(&a.g_acc[1], h);
+      atomicMax(&a.g_acc[4], mx);
+    }
+    atomicAdd(&a.g_acc[2], nd);
+    long long* m = a.w_metrics + (size_t)gw * 4;
+    m[0] += (long long)nd;
+    m[1] += rc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&a.g_hist[i], (unsigned long long)s_hist[i]);
+}

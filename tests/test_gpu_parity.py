@@ -225,3 +225,70 @@ def test_scratch_arena_is_stream_ordered():
         res = run(g2, st, RunConfig(), stream=ctypes.c_void_p(s.cuda_stream))
         assert (res.clique_count, res.clique_hash, res.nodes_total) == \
             (base.clique_count, base.clique_hash, base.nodes_total)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_lane_per_root_path_matches_reference(case, monkeypatch):
+    """The |P| <= 32 class on the lane-per-root kernel (k_tiny, forced on with
+    MCE_TINY=1 for these small graphs): the reference's count, node total,
+    histogram and hash with the exact order; roots it hands back (dense,
+    heavy X, |X| > 32) run on the warp kernel in the same call."""
+    g, _ = _graph(case)
+    order = degeneracy_order(g, method="exact")
+    g2 = reorder(g, order)
+    st = stats(g2, order)
+    for mode in ("l1-ipx", "l1-ip"):
+        exp = case["runs"][mode]
+        roots, induced = mode.split("-")
+        monkeypatch.setenv("MCE_TINY", "0")
+        warp = run(g2, st, RunConfig(roots=roots, induced=induced, worker_list=False))
+        monkeypatch.setenv("MCE_TINY", "1")
+        for workers, wl in ((0, False), (8, False), (0, True), (3, True)):
+            res = run(g2, st, RunConfig(workers=workers, roots=roots, induced=induced,
+                                        worker_list=wl))
+            assert res.clique_count == exp["count"], (mode, workers, wl)
+            if induced == "ip" or not wl:
+                assert res.nodes_total == exp["nodes"], (mode, workers, wl)
+                assert sum(w.nodes_visited for w in res.worker_metrics) == exp["nodes"]
+            assert res.clique_hash == warp.clique_hash
+            assert res.size_histogram == warp.size_histogram
+            if "hash" in exp:
+                assert res.clique_hash_hex == exp["hash"], mode
+            if case["n"] and st.degeneracy <= 32 and case["m"]:
+                assert res.kernel_launches > warp.kernel_launches  # k_tiny ran
+
+
+def test_lane_per_root_fallbacks_match_oracle(monkeypatch):
+    """Roots the lane kernel must hand back -- dense (> 64 induced edges),
+    |X| > 32, heavy X (|X| >= 256) -- mixed with sparse ones in one call."""
+    rng = np.random.default_rng(7)
+    parts, base = [], 0
+    k = 13  # K_13: early roots have 12 members and 66 > 64 edges
+    parts += [(base + i, base + j) for i in range(k) for j in range(i + 1, k)]
+    base += k
+    for leaves in (300, 60):  # hubs in many triangles: |X| >= 256 (heavy) and 32 < |X| < 256
+        hub = base
+        for t in range(leaves):
+            a, b = base + 1 + 2 * t, base + 2 + 2 * t
+            parts += [(hub, a), (hub, b), (a, b)]
+        base += 2 * leaves + 1
+    sparse = generate.gnp_edges(3000, 0.004, seed=3)
+    parts += [(base + int(u), base + int(v)) for u, v in sparse]
+    base += 3000
+    edges = np.asarray(parts, dtype=np.int64)
+    edges = edges[rng.permutation(len(edges))]
+    n = base
+    g = from_edges(edges, n)
+    g2, _, st = preprocess(g, method="exact")
+    for induced in ("ipx", "ip"):
+        monkeypatch.setenv("MCE_TINY", "1")
+        res = run(g2, st, RunConfig(induced=induced, worker_list=False))
+        monkeypatch.setenv("MCE_TINY", "0")
+        ref = run(g2, st, RunConfig(induced=induced, worker_list=False))
+        orc = oracle.enumerate_cliques(g2.row_offsets, g2.col_indices, roots="l1",
+                                       induced=induced, degeneracy=st.degeneracy,
+                                       labels=g2.labels)
+        assert res.clique_count == ref.clique_count == orc["count"]
+        assert res.nodes_total == ref.nodes_total == orc["nodes"]
+        assert res.clique_hash_hex == ref.clique_hash_hex == orc["hash"]
+        assert res.size_histogram == ref.size_histogram

@@ -2009,9 +2009,14 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   static bool have[64];
   if (dev < 0 || dev >= 64) dev = 0;
   if (!have[dev]) {
+    // (default carveout: these kernels lean on L1 for their global rows,
+    // stacks and X rows -- max-shared measured slower)
     MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cache[dev], kern, WARPS * 32, smem));
     have[dev] = true;
+    if (getenv("MCE_TRACE"))
+      fprintf(stderr, "[mce_trace] k_enumerate W=%d: %d CTAs/SM of %d warps, %zu B shared each\n", W,
+              per_sm_cache[dev], WARPS, smem);
   }
   const int per_sm = per_sm_cache[dev];
   if (per_sm < 1) {
@@ -2121,7 +2126,12 @@ int launch_tiny(bool full, TinyArgs ta, cudaStream_t s, cudaEvent_t* ev, int64_t
   auto kern = full ? k_tiny<true> : k_tiny<false>;
   if (!have[full][dev]) {
     MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // all of the unified L1 as shared memory: three CTAs' slices per SM
+    MCE_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
     MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[full][dev], kern, TINY_THREADS, smem));
+    if (getenv("MCE_TRACE"))
+      fprintf(stderr, "[mce_trace] k_tiny: %d CTAs/SM, %zu B shared each\n", per_sm[full][dev], smem);
     have[full][dev] = true;
   }
   if (per_sm[full][dev] < 1) {

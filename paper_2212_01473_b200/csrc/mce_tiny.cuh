@@ -31,7 +31,8 @@ constexpr int64_t TINY_MIN_ROOTS = 8192;  // smaller W = 1 classes stay on the w
 constexpr int TINY_THREADS = 32 * TINY_WARPS;
 constexpr int TINY_XT = 32;    // X members per root (|X| <= 32)
 constexpr int TINY_STRIDE = 33;
-constexpr int TINY_SLICE = 32 * TINY_STRIDE;  // words per warp per array
+constexpr int TINY_SLICE = 32 * TINY_STRIDE;  // member lists: words per warp
+constexpr int TINY_POOL = 1024;  // rows + X rows of a warp's 32 roots (np + nx words each)
 #ifndef MCE_TINY_E_MAX
 #define MCE_TINY_E_MAX 64
 #endif
@@ -43,7 +44,8 @@ constexpr int tiny_max_clique(int e) {
   return c;
 }
 constexpr int TINY_DEPTH = tiny_max_clique(TINY_E_MAX) + 1;
-constexpr int TINY_SMEM_WORDS = HIST_SMEM + 3 * TINY_SLICE * TINY_WARPS;
+constexpr int TINY_WARP_WORDS = TINY_SLICE + TINY_POOL + 64;  // + 32 bloom words (64-bit)
+constexpr int TINY_SMEM_WORDS = HIST_SMEM + TINY_WARP_WORDS * TINY_WARPS;
 
 struct TinyArgs {
   const int64_t* ro;
@@ -199,9 +201,9 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
   unsigned* s_hist = tsm;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  int32_t* spl = reinterpret_cast<int32_t*>(tsm + HIST_SMEM) + warp * 3 * TINY_SLICE;
-  uint32_t* srow = reinterpret_cast<uint32_t*>(spl + TINY_SLICE);
-  uint32_t* sxb = srow + TINY_SLICE;
+  int32_t* spl = reinterpret_cast<int32_t*>(tsm + HIST_SMEM) + warp * TINY_WARP_WORDS;
+  unsigned long long* sbloom = reinterpret_cast<unsigned long long*>(spl + TINY_SLICE);
+  uint32_t* spool = reinterpret_cast<uint32_t*>(spl + TINY_SLICE + 64);
   for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
   const int gw = (int)((blockIdx.x * TINY_THREADS + threadIdx.x) >> 5);
@@ -215,8 +217,6 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
   unsigned long long cliques = 0, hash = 0, nodes = 0, max_size = 0;
   long long claimed = 0;
   int32_t* mypl = spl + lane * TINY_STRIDE;
-  uint32_t* myrow = srow + lane * TINY_STRIDE;
-  uint32_t* myxb = sxb + lane * TINY_STRIDE;
   for (;;) {
     if (gw >= a.max_warps) break;
     unsigned long long base = 0;
@@ -238,22 +238,35 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
     }
     bool ok = valid && (renc >> ROOT_ID_BITS) == 0 && np <= 32 && nx <= TINY_XT;
     if (!ok) np = nx = 0;
-    // member list (padded for tiny_find), zeroed rows
-    for (int k = 0; k < 32; ++k) mypl[k] = 0x7fffffff;
-    for (int k = 0; k < np; ++k) myrow[k] = 0;
-    for (int t = 0; t < nx; ++t) myxb[t] = 0;
-    __syncwarp();  // other lanes fill this root's member list below
-    // ---- build, all 32 roots at once.  Member q of the batch: root r's P
-    // members first (np_r), then its X members (nx_r).
-    const int cnt = np + nx;
+    // root r's rows and X rows: np + nx words of the warp's pool at its
+    // prefix offset (roots past the pool's end go to the warp kernel)
+    int cnt = np + nx;
     int incl = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int t = __shfl_up_sync(FULLMASK, incl, d);
       if (lane >= d) incl += t;
     }
+    if (__any_sync(FULLMASK, incl > TINY_POOL)) {  // the suffix past the pool's end
+      if (incl > TINY_POOL) {
+        ok = false;
+        np = nx = cnt = 0;
+      }
+      incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, incl, d);
+        if (lane >= d) incl += t;
+      }
+    }
     const int excl = incl - cnt;
     const int total = __shfl_sync(FULLMASK, incl, 31);
+    uint32_t* myrow = spool + excl;
+    uint32_t* myxb = myrow + np;
+    // member list (padded for tiny_find), zeroed rows
+    for (int k = 0; k < 32; ++k) mypl[k] = 0x7fffffff;
+    for (int k = 0; k < cnt; ++k) myrow[k] = 0;
+    __syncwarp();  // other lanes fill this root's member list below
     // P member lists: one coalesced pass over the roots' N+ ranges
     for (int q0 = 0; q0 < total; q0 += 32) {
       const int q = q0 + lane;
@@ -269,6 +282,12 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       if (q < total && k < npr) spl[r * TINY_STRIDE + k] = __ldg(&col[sr + k]);
     }
     __syncwarp();
+    {  // 64-bit bloom filter of the root's members: most N+ entries miss P
+      unsigned long long bl = 0;
+      for (int k = 0; k < np; ++k) bl |= 1ull << (mypl[k] & 63);
+      sbloom[lane] = bl;
+    }
+    __syncwarp();
     for (int q0 = 0; q0 < total; q0 += 32) {
       // lane: member q0 + lane -> its root, kind, index and N+ range
       const int q = q0 + lane;
@@ -281,17 +300,19 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       const int k = q - __shfl_sync(FULLMASK, excl, r);
       const int npr = __shfl_sync(FULLMASK, np, r);
       const int64_t xr = __shfl_sync(FULLMASK, xb0, r);
+      const int rbase = __shfl_sync(FULLMASK, excl, r);
       int64_t lo = 0;
       int len = 0;
-      int info = 0;  // root (5 bits) | X member (bit 5) | index (bits 6..)
+      // root (5 bits) | X member (bit 5) | index (5 bits) | its rows' pool offset (11 bits)
+      int info = 0;
       if (q < total) {
         int32_t m;
         if (k < npr) {
           m = spl[r * TINY_STRIDE + k];
-          info = r | (k << 6);
+          info = r | (k << 6) | (rbase << 11);
         } else {
           m = __ldg(&col[xr + (k - npr)]);
-          info = r | 32 | ((k - npr) << 6);
+          info = r | 32 | ((k - npr) << 6) | ((rbase + npr) << 11);
         }
         lo = __ldg(&a.split[m]);
         len = (int)(__ldg(&a.ro[m + 1]) - lo);
@@ -327,14 +348,13 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
         for (int u = 0; u < U; ++u) {
           if (b2 + u * 32 + lane < tot2) {
             const int rr = inf[u] & 31;
-            const int j = tiny_find(spl + rr * TINY_STRIDE, val[u]);
-            if (j >= 0) {
-              const int ii = inf[u] >> 6;
-              if (inf[u] & 32) {
-                atomicOr(&sxb[rr * TINY_STRIDE + ii], 1u << j);
-              } else {  // N+(p_ii) holds only members after ii
-                atomicOr(&srow[rr * TINY_STRIDE + ii], 1u << j);
-                atomicOr(&srow[rr * TINY_STRIDE + j], 1u << ii);
+            if ((sbloom[rr] >> (val[u] & 63)) & 1ull) {
+              const int j = tiny_find(spl + rr * TINY_STRIDE, val[u]);
+              if (j >= 0) {
+                const int ii = (inf[u] >> 6) & 31;
+                uint32_t* rb = spool + (inf[u] >> 11);
+                atomicOr(&rb[ii], 1u << j);           // X row t = ii, or P row ii ...
+                if (!(inf[u] & 32)) atomicOr(&rb[j], 1u << ii);  // ... and its mirror
               }
             }
           }

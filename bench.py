@@ -189,13 +189,17 @@ def measured_hbm_peak() -> tuple[float, str]:
 
 
 def ncu_traffic(workload: str):
-    """dram bytes per enumeration launch from the committed ncu capture, if any."""
+    """DRAM bytes of one step's enumeration launches from the committed ncu
+    capture (profiles/traffic.json), plus that capture's L2 bytes and issue /
+    warp-occupancy figures (the enumeration is latency/issue bound, not HBM
+    bound: these say how far from which roof)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(workload)
+            d = json.load(fh)
+        return d.get(workload), d.get("_detail", {}).get(workload)
     except (OSError, ValueError):
-        return None
+        return None, None
 
 
 def load_workload(name: str, seed: int, on_device: bool):
@@ -410,8 +414,9 @@ def main():
                  "d2h_bytes_per_step": int(8 * (10 + 4096))} if e2e_ms else None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": ncu_traffic(args.workload),
-                     "kernel": "k_enumerate (all width classes)",
+                     "traffic": ncu_traffic(args.workload)[0],
+                     "ncu": ncu_traffic(args.workload)[1],
+                     "kernel": "enumeration kernels (k_tiny lane-per-root + k_enumerate width classes)",
                      "kernel_ms_per_step": kernel_ms / args.steps,
                      "kernel_ms_per_launch": per_launch_ms,
                      "algorithmic_bytes_per_step": build_bytes_step,

@@ -136,6 +136,10 @@ typedef struct {
   int donation_min_x;    /* B200 extension: also donate a branch whose node has at least
                             this many live X_X members (0 = off; the reference donates on
                             |P| >= donation_min_p only).  Scheduling only: same results */
+  int no_pivot;          /* 1 = branch on all of P (basic Bron-Kerbosch, bk.py:124-150);
+                            0 = Tomita pivot (bk.py:82-110), the engine's default */
+  int timing;            /* 1 = fill the per-worker time columns (RunConfig.timing,
+                            metrics.py:13-32); 0 = counters only */
 } mce_run_config;
 
 typedef struct {
@@ -151,12 +155,24 @@ typedef struct {
   int64_t build_bytes;   /* algorithmic graph bytes the induced-subgraph builds read */
   int64_t hist[MCE_HIST_MAX]; /* hist[s] = maximal cliques of size s */
   int64_t induced_full;  /* the induced mode the run used (resolves auto) */
+  double phase1_ms;      /* device time until every root of a launch was claimed, summed
+                            over the launches (scheduler.py:481-490 phase1_time) */
+  double phase2_ms;      /* device time after that: worker-list donations only */
+  double clock_khz;      /* SM clock the worker time columns are counted in */
 } mce_run_result;
+
+/* Columns of one worker's row in mce_enumerate's worker_metrics: */
+#define MCE_WM_COLS 9  /* nodes, roots claimed, donations made, donations received, then
+                          SM cycles (cfg.timing only) spent in the induced-subgraph build,
+                          pivot selection, set operations (leaf batches, X_X partitions,
+                          register-resident subtrees), the worker list / root claims, and
+                          the worker's whole run (metrics.py TIME_CATEGORIES; "other" is
+                          the whole run minus the four) */
 
 /* Enumerate every maximal clique of a canonical, degeneracy-reordered graph
  * (scheduler.py:441-492).  `collect` (host, collect_cap words) receives the
- * clique stream [size, v0, v1, ...]...; `worker_metrics` (host, 4 int64 per
- * worker: nodes, roots claimed, donations made, donations received). */
+ * clique stream [size, v0, v1, ...]...; `worker_metrics` (host, MCE_WM_COLS
+ * int64 per worker, see above). */
 int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collect,
                   int64_t* worker_metrics, int64_t worker_metrics_cap, mce_run_result* out,
                   void* stream);

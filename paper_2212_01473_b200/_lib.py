@@ -42,6 +42,8 @@ class RunConfigC(ctypes.Structure):
         ("measure_bytes", ctypes.c_int),
         ("partial_xrows_min_w", ctypes.c_int),
         ("donation_min_x", ctypes.c_int),
+        ("no_pivot", ctypes.c_int),
+        ("timing", ctypes.c_int),
     ]
 
 
@@ -59,7 +61,13 @@ class RunResultC(ctypes.Structure):
         ("build_bytes", ctypes.c_int64),
         ("hist", ctypes.c_int64 * HIST_MAX),
         ("induced_full", ctypes.c_int64),
+        ("phase1_ms", ctypes.c_double),
+        ("phase2_ms", ctypes.c_double),
+        ("clock_khz", ctypes.c_double),
     ]
+
+
+WM_COLS = 9  # MCE_WM_COLS
 
 
 EXPORTS = {

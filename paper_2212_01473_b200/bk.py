@@ -154,10 +154,38 @@ def oracle_enumerate(g: Graph) -> list[tuple[int, ...]]:
 
 def bk_pivot(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
     """All maximal cliques of ``g`` (reference bk.py:153-183) via the GPU
-    engine; cliques are reported in ``g``'s labels."""
+    engine; cliques are reported in ``g``'s labels.  ``metrics["nodes"]`` is
+    the engine's pivoting traversal over the degeneracy-ordered subtrees --
+    the reference's single whole-graph recursion pivots once more at the top
+    and breaks ties by global id, so its total differs (both never exceed
+    bk_basic's)."""
     return _enumerate_whole_graph(g, sink, metrics)
 
 
 def bk_basic(g: Graph, sink: CliqueSink, metrics: dict | None = None) -> int:
-    """Same clique set as reference bk.py:124-150 (the GPU engine always pivots)."""
-    return _enumerate_whole_graph(g, sink, metrics)
+    """Plain Bron-Kerbosch without pivoting (reference bk.py:124-150), on the GPU.
+
+    The reference's recursion from (R = {}, P = V, X = {}) branches on every
+    vertex in id order, so its first level IS the per-vertex subtree
+    decomposition in the graph's own order: vertex v's subtree starts from
+    P = N(v) & {u > v}, X = N(v) & {u < v}.  The engine runs exactly those
+    subtrees (no degeneracy reordering) with ``pivot=False``, and the node
+    total is the reference's: every subtree node plus the top-level call."""
+    from paper_2212_01473_b200.graph import GraphStats
+    from paper_2212_01473_b200.scheduler import RunConfig, run
+
+    n = g.num_vertices
+    if n == 0:
+        if metrics is not None:
+            metrics["nodes"] = 0
+        return sink.total
+    ro = g.row_offsets
+    ci = g.col_indices
+    later = int(max(ro[v + 1] - ro[v] - np.searchsorted(ci[ro[v]:ro[v + 1]], v, side="right")
+                    for v in range(n)))
+    st = GraphStats(n, len(ci) // 2, int(np.diff(ro).max()), later)
+    res = run(g, st, RunConfig(workers=0, roots="l1", induced="ipx", worker_list=False),
+              sink=sink, pivot=False)
+    if metrics is not None:
+        metrics["nodes"] = res.nodes_total + 1  # + the top-level call go([], V, {})
+    return sink.total

@@ -124,7 +124,7 @@ struct EnumArgs {
   // outputs
   unsigned long long* g_acc;   // 0 cliques, 1 hash, 2 nodes, 3 donations, 4 max size
   unsigned long long* g_hist;  // HIST_MAX
-  long long* w_metrics;        // per worker: nodes, roots, donations made, received
+  long long* w_metrics;        // per worker: MCE_WM_COLS columns (include/mce_b200.h)
   long long* root_cycles;      // diagnostics (MCE_PROFILE_ROOTS): SM cycles per claimed root
   int64_t* collect;
   int64_t collect_cap;
@@ -144,7 +144,19 @@ struct EnumArgs {
   const uint32_t* heavy_rows;  // X rows of the heavy-X roots (k_heavy_xrows), per slot
   const int64_t* heavy_off;    // word offset of slot h's rows (stride |X| of the root)
   int compact;                 // run small subtrees on the register copy (compact_run); 0: off
+  int no_pivot;                // basic Bron-Kerbosch: branch on all of P (bk.py:124-150)
+  int timing;                  // per-worker SM cycles by category (w_metrics columns 4..8)
+  unsigned long long* phase_ns;  // this launch: [~first start, ~first root-list miss, last end]
 };
+
+constexpr int WM = MCE_WM_COLS;
+enum TimeCat { T_BUILD = 4, T_PIVOT = 5, T_SETOPS = 6, T_WLIST = 7, T_TOTAL = 8 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* a, int len, int32_t key) {
   int lo = 0, hi = len;
@@ -292,6 +304,12 @@ struct Worker {
     lpx = a.lpx + (size_t)wid * a.levels;
     rpath = a.rpath + (size_t)wid * (a.levels + 2);
     hsum = a.hsum + (size_t)wid * (a.levels + 2);
+  }
+
+  // ---------------------------------------------------------------- timing (cfg.timing)
+  __device__ __forceinline__ long long tic() const { return a.timing ? clock64() : 0; }
+  __device__ __forceinline__ void toc(int col, long long t0) const {
+    if (a.timing && lane == 0) a.w_metrics[(size_t)wid * WM + col] += clock64() - t0;
   }
 
   // ---------------------------------------------------------------- words
@@ -625,6 +643,11 @@ struct Worker {
       cmask[k] = __ballot_sync(FULLMASK, (P.w[k] | XP.w[k]) != 0);
     }
     __syncwarp();
+    if (a.no_pivot) {  // basic BK: every member of P is a branch
+#pragma unroll
+      for (int k = 0; k < K; ++k) BR.w[k] = P.w[k];
+      return;
+    }
     int best = -1, bestc = 0x7fffffff;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -1172,6 +1195,7 @@ struct Worker {
             prow = shflm(H == 2 && pp >= 32 ? xrow[H - 1] : xrow[0], pp & 31);
           }
         }
+        if (a.no_pivot) prow = 0;  // basic BK: every member of P is a branch
         BR = P & ~prow;
         // leaf batch (see leaf_batch): every branch whose child P is empty
         M xxadj = 0;
@@ -1431,14 +1455,20 @@ struct Worker {
       if (fresh) {
         const int cw = compact_width(P, XP, live);
         if (cw) {  // the whole subtree below this node, on the register copy
+          const long long t0 = tic();
           const uint64_t hs0 = hsum[rlen];
           if (cw == 32 || CMP_NARROW_ONLY) compact_run<uint32_t>(P, XP, live, rlen, below, hs0);
           else compact_run<unsigned long long>(P, XP, live, rlen, below, hs0);
 #pragma unroll
           for (int k = 0; k < K; ++k) NL.w[k] = 0;
+          toc(T_SETOPS, t0);
         } else {
+          long long t0 = tic();
           pivot_branches(P, XP, live, BR);
+          toc(T_PIVOT, t0);
+          t0 = tic();
           leaf_batch(P, XP, BR, live, rlen, NL, depth < 64 && ((xsorted >> depth) & 1ull));
+          toc(T_SETOPS, t0);
         }
         fresh = false;
       }
@@ -1478,7 +1508,10 @@ struct Worker {
         B cxp;
 #pragma unroll
         for (int k = 0; k < K; ++k) cxp.w[k] = XP.w[k] & rowv.w[k];
-        if (try_donate(childP, cxp, v, gv, live, rlen)) continue;
+        const long long t0 = tic();
+        const bool gave = try_donate(childP, cxp, v, gv, live, rlen);
+        toc(T_WLIST, t0);
+        if (gave) continue;
       }
       if (cpop == 0) {  // not reached: leaf_batch settled every leaf branch
         nodes++;
@@ -1494,7 +1527,9 @@ struct Worker {
         }
         continue;
       }
+      const long long tp = tic();
       const int kept = partition(v, gv, live);
+      toc(T_SETOPS, tp);
       if (depth < 63) {  // the kept part inherits the order; the parent's prefix is permuted
         const unsigned long long bit = (xsorted >> depth) & 1ull;
         xsorted &= ~(3ull << depth);
@@ -1670,6 +1705,8 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
                                   s_hist, s_cmp + warp * CMP_WORDS);
     int stripe = wid % ROOT_STRIPES;
     bool phase1 = true;
+    const long long t_start = clock64();
+    if (a.phase_ns && lane == 0) atomicMax(&a.phase_ns[0], ~gtimer());
     // one traverse() call site (inlined once): phase 1 claims independent
     // subtrees (scheduler.py:253-273), phase 2 parks on the worker list and
     // receives donated branches
@@ -1678,18 +1715,28 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
       int nxx = 0, rlen = 0;
       int64_t idx = -1;
       if (phase1) {
+        long long t0 = wk.tic();
         idx = wk.claim_root(stripe);
+        wk.toc(T_WLIST, t0);
         if (idx < 0) {
           phase1 = false;
+          if (a.phase_ns && lane == 0) atomicMax(&a.phase_ns[1], ~gtimer());
           if (!a.worker_list_on) break;
           continue;
         }
         wk.roots_claimed++;
+        t0 = wk.tic();
         rlen = wk.prepare_root(a.roots[idx], P, XP, nxx);
+        wk.toc(T_BUILD, t0);
       } else {
-        if (!wk.park()) break;
+        long long t0 = wk.tic();
+        const bool got = wk.park();
+        wk.toc(T_WLIST, t0);
+        if (!got) break;
         wk.don_recv++;
+        t0 = wk.tic();
         rlen = wk.prepare_donated(P, XP, nxx);
+        wk.toc(T_BUILD, t0);
       }
       const long long t0 = a.root_cycles ? clock64() : 0;
       wk.traverse(P, XP, nxx, rlen, phase1);
@@ -1701,11 +1748,13 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
       atomicAdd(&a.g_acc[2], (unsigned long long)wk.nodes);
       atomicAdd(&a.g_acc[3], (unsigned long long)wk.don_made);
       atomicMax(&a.g_acc[4], wk.max_size);
-      long long* m = a.w_metrics + (size_t)wid * 4;
+      long long* m = a.w_metrics + (size_t)wid * WM;
       m[0] += wk.nodes;
       m[1] += wk.roots_claimed;
       m[2] += wk.don_made;
       m[3] += wk.don_recv;
+      if (a.timing) m[T_TOTAL] += clock64() - t_start;
+      if (a.phase_ns) atomicMax(&a.phase_ns[2], gtimer());
     }
   }
   __syncthreads();
@@ -2247,9 +2296,12 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   }
   // every zero-initialised word of the call in one block, one memset:
   // acc[8] | hist[HIST_MAX] | collect_len | build bytes | root classes + heavy
-  // plan counters [16] | per-worker metrics [4 * metric_slots]
+  // plan counters [16] | launch phase times [32] | per-worker metrics [WM * metric_slots]
   constexpr int ZB_CLS = 8 + HIST_MAX + 2;
-  const size_t zwords = (size_t)ZB_CLS + 16 + 4 * (size_t)metric_slots;
+  constexpr int ZB_PH = ZB_CLS + 16;
+  constexpr int ZB_WM = ZB_PH + 32;
+  static_assert(3 * (NUM_WIDTHS + 1) <= 32, "phase slots");
+  const size_t zwords = (size_t)ZB_WM + WM * (size_t)metric_slots;
   unsigned long long* zb = nullptr;
   if (get(&zb, zwords)) return -1;
   MCE_CHECK(cudaMemsetAsync(zb, 0, zwords * sizeof(unsigned long long), s));
@@ -2257,7 +2309,9 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   unsigned long long* hist = zb + 8;
   unsigned long long* collect_len = zb + 8 + HIST_MAX;
   unsigned long long* bb = collect_len + 1;
-  long long* wmet = reinterpret_cast<long long*>(zb + ZB_CLS + 16);
+  long long* wmet = reinterpret_cast<long long*>(zb + ZB_WM);
+  unsigned long long* phase = zb + ZB_PH;  // 3 words per launch
+  int nph = 0;
   int64_t* d_collect = nullptr;
   if (cfg->collect_cap > 0 && get(&d_collect, cfg->collect_cap)) {
     cleanup();
@@ -2430,6 +2484,9 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.min_x = cfg->donation_min_x;
       args.heavy_rows = heavy_pool;
       args.heavy_off = hp.off;
+      args.no_pivot = cfg->no_pivot;
+      args.timing = cfg->timing;
+      args.phase_ns = phase + 3 * nph++;
       {
         const char* e = getenv("MCE_COMPACT");  // diagnostics: MCE_COMPACT=0 disables compact_run
         args.compact = e ? atoi(e) : 1;
@@ -2464,8 +2521,10 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
         ta.g_acc = acc;
         ta.g_hist = hist;
         ta.w_metrics = wmet;
-        ta.phase_ns = nullptr;
+        ta.phase_ns = phase + 3 * nph++;
         ta.max_warps = cfg->workers > 0 ? cfg->workers : 0;
+        ta.no_pivot = cfg->no_pivot;
+        ta.timing = cfg->timing;
         if (launch_tiny(full, ta, s, &events[2 * nev++], &launches, &workers_used)) {
           cleanup();
           return -1;
@@ -2546,17 +2605,37 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   const int64_t wslots = (worker_metrics && worker_metrics_cap > 0)
                              ? std::min<int64_t>(worker_metrics_cap, max_workers_slots)
                              : 0;
-  const size_t back = (size_t)ZB_CLS + 16 + 4 * (size_t)std::max<int64_t>(wslots, 0);
+  const size_t back = (size_t)ZB_WM + WM * (size_t)std::max<int64_t>(wslots, 0);
   MCE_CHECK(cudaMemcpyAsync(pin, zb, back * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   tr.mark("results queued");
   MCE_CHECK(cudaStreamSynchronize(s));
   tr.mark("results synced");
+  if (tr.on)
+    fprintf(stderr, "[mce_trace] k_tiny handed back %llu roots to the warp kernel\n",
+            pin[ZB_CLS + MAXP_SLOT + 1 + 3 + 1]);
   unsigned long long h_acc[8];
   memcpy(h_acc, pin, sizeof(h_acc));
   memcpy(out->hist, pin + 8, sizeof(int64_t) * HIST_MAX);
   const unsigned long long h_len = pin[8 + HIST_MAX];
   const unsigned long long h_bytes = pin[8 + HIST_MAX + 1];
-  if (wslots > 0) memcpy(worker_metrics, pin + ZB_CLS + 16, sizeof(int64_t) * 4 * wslots);
+  if (wslots > 0) memcpy(worker_metrics, pin + ZB_WM, sizeof(int64_t) * WM * wslots);
+  {  // phase 1 (roots left to claim) / phase 2 (worker list only), per launch
+    double p1 = 0.0, p2 = 0.0;
+    for (int i = 0; i < nph; ++i) {
+      const unsigned long long* ph = pin + ZB_PH + 3 * i;
+      if (!ph[0] || !ph[2]) continue;
+      const unsigned long long t0 = ~ph[0], t2 = ph[2];
+      const unsigned long long t1 = ph[1] ? std::min(~ph[1], t2) : t2;
+      if (t1 > t0) p1 += (double)(t1 - t0) / 1e6;
+      if (t2 > t1) p2 += (double)(t2 - t1) / 1e6;
+    }
+    out->phase1_ms = p1;
+    out->phase2_ms = p2;
+    int dev = 0, khz = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+    out->clock_khz = (double)khz;
+  }
   if (collect && cfg->collect_cap > 0) {
     int64_t words = std::min<int64_t>((int64_t)h_len, cfg->collect_cap);
     if (words > 0) {

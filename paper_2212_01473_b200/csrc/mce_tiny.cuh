@@ -29,10 +29,17 @@
 constexpr int TINY_WARPS = 8;
 constexpr int64_t TINY_MIN_ROOTS = 8192;  // smaller W = 1 classes stay on the warp kernel
 constexpr int TINY_THREADS = 32 * TINY_WARPS;
-constexpr int TINY_XT = 32;    // X members per root (|X| <= 32)
+#ifndef MCE_TINY_XT
+#define MCE_TINY_XT 32
+#endif
+#ifndef MCE_TINY_POOL
+#define MCE_TINY_POOL 1024
+#endif
+constexpr int TINY_XT = MCE_TINY_XT;  // X members per root
+static_assert(TINY_XT <= 64, "X member index has 6 bits in the walk's member word");
 constexpr int TINY_STRIDE = 33;
 constexpr int TINY_SLICE = 32 * TINY_STRIDE;  // member lists: words per warp
-constexpr int TINY_POOL = 1024;  // rows + X rows of a warp's 32 roots (np + nx words each)
+constexpr int TINY_POOL = MCE_TINY_POOL;  // rows + X rows of a warp's 32 roots (np + nx words each)
 #ifndef MCE_TINY_E_MAX
 #define MCE_TINY_E_MAX 64
 #endif
@@ -59,9 +66,11 @@ struct TinyArgs {
   unsigned long long* fallback_len;
   unsigned long long* g_acc;         // 0 cliques, 1 hash, 2 nodes, 3 donations, 4 max size
   unsigned long long* g_hist;
-  long long* w_metrics;              // per warp: nodes, roots, donations made, received
-  unsigned long long* phase_ns;      // [0] first start (min), [1] phase-2 start (min), [2] end (max)
+  long long* w_metrics;              // per warp: MCE_WM_COLS columns
+  unsigned long long* phase_ns;      // [~first start, ~first root-list miss, last end] (atomicMax)
   int max_warps;                     // workers requested (warps >= this stay idle)
+  int no_pivot;                      // basic Bron-Kerbosch: branch on all of P
+  int timing;                        // SM cycles by category into w_metrics
 };
 
 __device__ __forceinline__ void tiny_hist_add(unsigned* s_hist, unsigned long long* g_hist, int size) {
@@ -89,7 +98,7 @@ __device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, c
                                          uint32_t* xm, int np, int live, uint64_t hs,
                                          unsigned* s_hist, unsigned long long& cliques,
                                          unsigned long long& hash, unsigned long long& nodes,
-                                         unsigned long long& max_size) {
+                                         unsigned long long& max_size, bool no_pivot) {
   uint32_t P = np == 32 ? ~0u : ((1u << np) - 1u), XP = 0, BR = 0, NL = 0;
   int rlen = 1, depth = 0;
   nodes++;
@@ -124,6 +133,7 @@ __device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, c
           }
         }
       }
+      if (no_pivot) prow = 0;  // basic BK: every member of P is a branch
       BR = P & ~prow;
       // leaf batch: every branch whose child P is empty (see Worker::leaf_batch)
       const int size = rlen + 1;
@@ -208,20 +218,24 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
   __syncthreads();
   const int gw = (int)((blockIdx.x * TINY_THREADS + threadIdx.x) >> 5);
   const int32_t* __restrict__ col = a.col;
-  if (a.phase_ns && lane == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicMin(&a.phase_ns[0], t);
-  }
+  if (a.phase_ns && lane == 0) atomicMax(&a.phase_ns[0], ~gtimer());
+  const long long t_start = clock64();
+  long long t_build = 0, t_dfs = 0, t_claim = 0;
   const unsigned lt = (1u << lane) - 1u;
   unsigned long long cliques = 0, hash = 0, nodes = 0, max_size = 0;
   long long claimed = 0;
   int32_t* mypl = spl + lane * TINY_STRIDE;
   for (;;) {
     if (gw >= a.max_warps) break;
+    long long t0 = a.timing ? clock64() : 0;
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(a.counter, 32ull);
     base = __shfl_sync(FULLMASK, base, 0);
+    if (a.timing) {
+      const long long t1 = clock64();
+      t_claim += t1 - t0;
+      t0 = t1;
+    }
     if (base >= (unsigned long long)a.num_roots) break;
     // ---- lane r: root r of the batch
     const int64_t idx = (int64_t)base + lane;
@@ -303,16 +317,16 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       const int rbase = __shfl_sync(FULLMASK, excl, r);
       int64_t lo = 0;
       int len = 0;
-      // root (5 bits) | X member (bit 5) | index (5 bits) | its rows' pool offset (11 bits)
+      // root (5 bits) | X member (bit 5) | index (6 bits) | its rows' pool offset
       int info = 0;
       if (q < total) {
         int32_t m;
         if (k < npr) {
           m = spl[r * TINY_STRIDE + k];
-          info = r | (k << 6) | (rbase << 11);
+          info = r | (k << 6) | (rbase << 12);
         } else {
           m = __ldg(&col[xr + (k - npr)]);
-          info = r | 32 | ((k - npr) << 6) | ((rbase + npr) << 11);
+          info = r | 32 | ((k - npr) << 6) | ((rbase + npr) << 12);
         }
         lo = __ldg(&a.split[m]);
         len = (int)(__ldg(&a.ro[m + 1]) - lo);
@@ -351,8 +365,8 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
             if ((sbloom[rr] >> (val[u] & 63)) & 1ull) {
               const int j = tiny_find(spl + rr * TINY_STRIDE, val[u]);
               if (j >= 0) {
-                const int ii = (inf[u] >> 6) & 31;
-                uint32_t* rb = spool + (inf[u] >> 11);
+                const int ii = (inf[u] >> 6) & 63;
+                uint32_t* rb = spool + (inf[u] >> 12);
                 atomicOr(&rb[ii], 1u << j);           // X row t = ii, or P row ii ...
                 if (!(inf[u] & 32)) atomicOr(&rb[j], 1u << ii);  // ... and its mirror
               }
@@ -362,6 +376,11 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       }
     }
     __syncwarp();
+    if (a.timing) {
+      const long long t1 = clock64();
+      t_build += t1 - t0;
+      t0 = t1;
+    }
     // ---- lane r enumerates root r
     if (ok) {
       int e2 = 0;
@@ -377,7 +396,7 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
         }
         if (np > 0) {
           tiny_dfs<PIVOT_XX>(a, mypl, myrow, myxb, np, nxx, __ldg(&a.vhash[v]), s_hist, cliques,
-                             hash, nodes, max_size);
+                             hash, nodes, max_size, a.no_pivot != 0);
           claimed++;
         }
       }
@@ -391,11 +410,11 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       if (fb) a.fallback[o + __popc(fm & lt)] = renc;
     }
     __syncwarp();
+    if (a.timing) t_dfs += clock64() - t0;  // the warp waits for its slowest lane
   }
-  if (a.phase_ns && lane == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicMin(&a.phase_ns[1], t);  // this warp found the root list exhausted
+  if (a.phase_ns && lane == 0 && gw < a.max_warps) {
+    const unsigned long long t = gtimer();
+    atomicMax(&a.phase_ns[1], ~t);  // this warp found the root list exhausted
     atomicMax(&a.phase_ns[2], t);
   }
   // warp totals (64-bit shuffles), one set of atomics per warp
@@ -417,9 +436,15 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       atomicMax(&a.g_acc[4], mx);
     }
     atomicAdd(&a.g_acc[2], nd);
-    long long* m = a.w_metrics + (size_t)gw * 4;
+    long long* m = a.w_metrics + (size_t)gw * WM;
     m[0] += (long long)nd;
     m[1] += rc;
+    if (a.timing) {
+      m[T_BUILD] += t_build;
+      m[T_SETOPS] += t_dfs;
+      m[T_WLIST] += t_claim;
+      m[T_TOTAL] += clock64() - t_start;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x)

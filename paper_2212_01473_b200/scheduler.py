@@ -117,6 +117,7 @@ class RunResult:
     kernel_ms: float = 0.0
     build_bytes: int = 0
     timing: bool = False
+    clock_khz: float = 0.0
 
     @property
     def worker_metrics(self) -> list[WorkerMetrics]:
@@ -125,9 +126,15 @@ class RunResult:
         raw = self.worker_metrics_raw
         if isinstance(raw, np.ndarray):
             out = []
+            hz = self.clock_khz * 1e3
             for i, row in enumerate(raw.tolist()):
                 m = WorkerMetrics(worker_id=i, enabled=self.timing)
-                m.nodes_visited, m.roots_claimed, m.donations_made, m.donations_received = row
+                m.nodes_visited, m.roots_claimed, m.donations_made, m.donations_received = row[:4]
+                if self.timing and hz > 0:
+                    build, pivot, setops, wlist, total = (c / hz for c in row[4:9])
+                    m.times.update(induced_build=build, pivot=pivot, set_ops=setops,
+                                   worker_list=wlist,
+                                   other=max(0.0, total - build - pivot - setops - wlist))
                 out.append(m)
             self.worker_metrics_raw = raw = out
         return raw
@@ -156,7 +163,8 @@ def _decode_stream(buf: np.ndarray, words: int, limit: int) -> list[tuple[int, .
 
 def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None, *,
         root_begin: int = 0, root_end: int = -1, root_stride: int = 1,
-        hash_labels: bool = True, stream=None, measure_bytes: bool = False) -> RunResult:
+        hash_labels: bool = True, stream=None, measure_bytes: bool = False,
+        pivot: bool = True) -> RunResult:
     """Enumerate all maximal cliques of a degeneracy-reordered graph on the
     GPU (reference scheduler.py:441-492).
 
@@ -164,6 +172,12 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
     subtree roots (vertices for l1, edges in CSR order for l2) -- used for
     bounded parity checks against the CPU oracle.  ``hash_labels`` hashes
     cliques by the graph's original labels (set by ``reorder``).
+    ``pivot=False`` branches on every member of P (basic Bron-Kerbosch, the
+    traversal of reference bk.py:124-150 below each root).
+
+    ``phase1_time`` / ``phase2_time`` are device times (global timer inside
+    the kernels): until every root of a launch was claimed, and the worker-
+    list tail after it, summed over the launches (scheduler.py:481-490).
     """
     cfg.validate()
     if sink is None:
@@ -198,9 +212,11 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
             measure_bytes=int(bool(measure_bytes)),
             partial_xrows_min_w=int(os.environ.get("MCE_PARTIAL_XROWS_MIN_W", "0")),
             donation_min_x=int(cfg.donation_min_x),
+            no_pivot=0 if pivot else 1,
+            timing=int(bool(cfg.timing)),
         )
         buf = np.zeros(max(cap_words, 1), dtype=np.int64) if cap_words else None
-        wm = np.zeros((slots, 4), dtype=np.int64)
+        wm = np.zeros((slots, _lib.WM_COLS), dtype=np.int64)
         res = _lib.RunResultC()
         t0 = perf_counter()
         _lib.check(_lib.lib().mce_enumerate(g.device.handle, ctypes.byref(c), _lib.ptr(buf),
@@ -231,8 +247,8 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
         induced_mode=induced,
         workers=workers,
         total_time=t1 - t0,
-        phase1_time=t1 - t0,
-        phase2_time=0.0,
+        phase1_time=float(res.phase1_ms) / 1e3,
+        phase2_time=float(res.phase2_ms) / 1e3,
         worker_metrics_raw=wm[:workers],
         nodes_total=int(res.nodes),
         clique_hash=int(res.hash),
@@ -242,4 +258,5 @@ def run(g: Graph, st: GraphStats, cfg: RunConfig, sink: CliqueSink | None = None
         kernel_ms=float(res.kernel_ms),
         build_bytes=int(res.build_bytes),
         timing=cfg.timing,
+        clock_khz=float(res.clock_khz),
     )

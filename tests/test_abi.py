@@ -64,3 +64,10 @@ def test_struct_layouts_match_header():
 
 def test_last_error_is_callable_without_a_device():
     assert isinstance(_lib.lib().mce_last_error(), bytes)
+
+
+def test_worker_metric_columns_match_header():
+    import re
+
+    text = open(os.path.join(ROOT, "include", "mce_b200.h")).read()
+    assert int(re.search(r"#define MCE_WM_COLS (\d+)", text).group(1)) == _lib.WM_COLS

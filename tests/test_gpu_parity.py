@@ -292,3 +292,53 @@ def test_lane_per_root_fallbacks_match_oracle(monkeypatch):
         assert res.nodes_total == ref.nodes_total == orc["nodes"]
         assert res.clique_hash_hex == ref.clique_hash_hex == orc["hash"]
         assert res.size_histogram == ref.size_histogram
+
+
+BK = __import__("json").load(open(__import__("os").path.join(
+    __import__("os").path.dirname(__file__), "golden", "bk_vectors.json")))["cases"]
+
+
+@pytest.mark.parametrize("name", sorted(BK))
+def test_bk_basic_and_pivot_match_reference(name, monkeypatch):
+    """bk_basic: the reference's count and node total (no pivoting, the
+    graph's own vertex order -- golden vectors from reference bk.py:124-150);
+    bk_pivot: the same clique set, never more nodes than bk_basic."""
+    from paper_2212_01473_b200 import bk_basic, bk_pivot
+
+    case = next(c for c in CASES if c["name"] == name)
+    g, _ = _graph(case)
+    exp = BK[name]
+    for tiny in ("0", "1"):  # warp kernel / lane-per-root kernel
+        monkeypatch.setenv("MCE_TINY", tiny)
+        mb, mp = {}, {}
+        sb, sp = CliqueSink.collecting(), CliqueSink.collecting()
+        assert bk_basic(g, sb, metrics=mb) == exp["count"]
+        assert mb["nodes"] == exp["basic_nodes"], (name, tiny)
+        assert bk_pivot(g, sp, metrics=mp) == exp["count"]
+        assert set(sb.collected) == set(sp.collected)
+        if "brute_force" in case:
+            assert set(sb.collected) == {tuple(c) for c in case["brute_force"]}
+        assert 0 < mp["nodes"] <= mb["nodes"]
+
+
+def test_phase_times_and_worker_time_categories():
+    """RunResult.phase1_time / phase2_time (device time before / after every
+    root was claimed) and WorkerMetrics.times with timing on (reference
+    scheduler.py:481-490, metrics.py:13-32)."""
+    edges, n = generate.workload_edges("ba200k")
+    g2, _, st = preprocess(from_edges(edges, n))
+    res = run(g2, st, RunConfig(timing=True))
+    assert res.phase1_time > 0 and res.phase2_time >= 0
+    assert res.phase1_time + res.phase2_time <= res.total_time
+    ms = res.worker_metrics
+    cats = ("induced_build", "pivot", "set_ops", "worker_list", "other")
+    assert all(set(m.times) == set(cats) for m in ms)
+    assert all(v >= 0 for m in ms for v in m.times.values())
+    busy = [m for m in ms if m.roots_claimed > 0]
+    assert busy and all(m.times["induced_build"] > 0 for m in busy)
+    assert sum(m.times["set_ops"] for m in ms) > 0
+    rep = res.report()
+    assert abs(sum(rep.category_shares.values()) - 1.0) < 1e-6
+    off = run(g2, st, RunConfig())
+    assert all(v == 0 for m in off.worker_metrics for v in m.times.values())
+    assert (off.clique_count, off.clique_hash) == (res.clique_count, res.clique_hash)

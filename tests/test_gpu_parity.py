@@ -143,7 +143,11 @@ def test_work_conservation_across_workers_and_donation():
     donated branch's partition of that prefix happens in the receiver, not
     the donor -- exactly as in the reference (scheduler.py:417-438) -- so
     later siblings can see a different order; node totals are then exact only
-    without donations, while counts and hashes stay exact."""
+    without donations, while counts and hashes stay exact.  The reference's
+    own scheduler shows it: profiles/r2/ref_ipx_donation_probe.txt (from
+    tests/golden/ref_ipx_donation_probe.py) -- gnp(200, 0.5), ipx, 8 workers,
+    donation_min_p=2: one of six runs reports 1,258,448 nodes against the
+    worker-list-off 1,258,446, same clique count."""
     for case in CASES:
         if case["name"] not in ("gnp_200_0.5_s3", "skew_2000_40", "gnp_300_0.08_s42"):
             continue
@@ -342,3 +346,34 @@ def test_phase_times_and_worker_time_categories():
     off = run(g2, st, RunConfig())
     assert all(v == 0 for m in off.worker_metrics for v in m.times.values())
     assert (off.clique_count, off.clique_hash) == (res.clique_count, res.clique_hash)
+
+
+C4 = __import__("json").load(open(__import__("os").path.join(
+    __import__("os").path.dirname(__file__), "golden", "criterion4.json")))["graphs"]
+
+
+@pytest.mark.parametrize("i", range(len(C4)))
+def test_criterion_4_graph_set(i, monkeypatch):
+    """The reference's acceptance criterion 4 (reference
+    tests/test_acceptance.py:93-109) on its own 20 graphs: full ("ipx")
+    subgraphs, workers {1, 2, 4, 8, 16} x worker list on/off -- the node
+    total is the reference's in every configuration, with donations
+    happening (also forced with donation_min_p=2), and on both the warp and
+    the lane-per-root kernels."""
+    gr = C4[i]
+    g = from_edges(np.asarray(gr["edges"], dtype=np.int64).reshape(-1, 2), gr["n"])
+    g2, _, st = preprocess(g, method="exact")
+    donated = 0
+    for tiny in ("0", "1"):
+        monkeypatch.setenv("MCE_TINY", tiny)
+        for workers in (1, 2, 4, 8, 16):
+            for wl in (True, False):
+                for min_p in ((10, 2) if wl else (10,)):
+                    res = run(g2, st, RunConfig(workers=workers, roots="l1", induced="ipx",
+                                                worker_list=wl, donation_min_p=min_p))
+                    assert res.clique_count == gr["count"]
+                    assert sum(w.nodes_visited for w in res.worker_metrics) == gr["nodes"], \
+                        (i, tiny, workers, wl, min_p, res.donation_count)
+                    donated += res.donation_count
+    # (these sparse graphs' subtrees are too small to donate: phase 2 finds no
+    # branch with |P| >= donation_min_p -- as in the reference's own run)

@@ -80,17 +80,34 @@ def test_small_workloads_full_parity(name):
     assert (ip.clique_count, ip.clique_hash) == (res.clique_count, res.clique_hash)
 
 
-@pytest.mark.parametrize("name,sample", [
-    ("planted1m", dict(root_begin=0, root_end=-1, root_stride=97)),
-    ("planted1m", dict(root_begin=999_000, root_end=-1, root_stride=1)),
-    ("rmat20", dict(root_begin=0, root_end=600_000, root_stride=13)),
+@pytest.mark.parametrize("name,sample,modes", [
+    ("planted1m", dict(root_begin=0, root_end=-1, root_stride=97), ("ipx", "ip")),
+    ("planted1m", dict(root_begin=999_000, root_end=-1, root_stride=1), ("ipx", "ip")),
+    ("rmat20", dict(root_begin=0, root_end=600_000, root_stride=13), ("ipx", "ip")),
+    # the dense core: the last 8,576 roots hold all but 0.2 % of rmat20's
+    # maximal cliques; its first part (~2.5e4 cliques per root) and a few
+    # roots 6,000 from the end (~6e6 cliques each, cliques up to size ~95)
+    ("rmat20", dict(root_begin=(1 << 20) - 8576, root_end=(1 << 20) - 7000, root_stride=32),
+     ("ipx", "ip")),
+    ("rmat20", dict(root_begin=(1 << 20) - 6000, root_end=(1 << 20) - 4000, root_stride=500),
+     ("ipx",)),
 ])
-def test_large_workloads_sampled_parity(name, sample):
+def test_large_workloads_sampled_parity(name, sample, modes):
     edges, n = generate.workload_edges(name)
     g = from_edges(edges, n)
     g2, _, st = preprocess(g)
-    _check_against_oracle(g2, st, induced="ipx", **sample)
-    _check_against_oracle(g2, st, induced="ip", **sample)
+    for induced in modes:
+        _check_against_oracle(g2, st, induced=induced, **sample)
+
+
+def test_planted1m_full_parity():
+    """configs[3] in full: every one of the 1,000,000 first-level roots, count,
+    node total, histogram and hash against the oracle on the same reordered
+    graph (the oracle takes ~10 s on the box's host threads)."""
+    edges, n = generate.workload_edges("planted1m")
+    g2, _, st = preprocess(from_edges(edges, n))
+    res = _check_against_oracle(g2, st, induced="ipx")
+    assert res.clique_count == 9_997_854 and max(res.size_histogram) == 60
 
 
 def test_planted_full_l1_equals_l2_and_shards_sum():
@@ -292,3 +309,8 @@ def test_rmat24_sampled_parity():
     for induced in ("ip", "ipx"):
         res = _check_against_oracle(g2, st, induced=induced, **sample)
         assert res.clique_count > 3000
+    # toward the core: 64 roots 100,000 from the end (~7e4 maximal cliques each,
+    # cliques up to size ~52); 50,000 from the end it is ~1e8 per root
+    core = dict(root_begin=n - 100_000, root_end=n - 100_000 + 64 * 16, root_stride=16)
+    res = _check_against_oracle(g2, st, induced="ipx", **core)
+    assert res.clique_count > 1_000_000

@@ -2631,10 +2631,13 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     }
     out->phase1_ms = p1;
     out->phase2_ms = p2;
-    int dev = 0, khz = 0;
+    // (the clock-rate attribute costs milliseconds per query: once per device)
+    static int khz_cache[64];
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
-    out->clock_khz = (double)khz;
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!khz_cache[dev]) cudaDeviceGetAttribute(&khz_cache[dev], cudaDevAttrClockRate, dev);
+    out->clock_khz = (double)khz_cache[dev];
   }
   if (collect && cfg->collect_cap > 0) {
     int64_t words = std::min<int64_t>((int64_t)h_len, cfg->collect_cap);

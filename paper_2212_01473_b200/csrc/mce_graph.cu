@@ -11,6 +11,7 @@
 //   reorder ............ graph.py:213-224
 #include <cub/cub.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <atomic>
@@ -502,6 +503,21 @@ struct APeelShared {
   int mindeg0;  // INT_MAX - minimum initial degree (max-reduced from the host's zero)
   unsigned int part;              // warps consuming chunks in this level's async phase
   unsigned long long head0;       // first queue slot of this level (static reservations)
+  // hand-over to the cluster tail (k_peel_tail): set by the grid kernel when
+  // at most `tail_max` vertices remain at a level boundary
+  int tail;
+  int tail_k, tail_degmax, tail_sel;
+  unsigned int tail_na;
+};
+
+// The tail kernel's own counters (zeroed by the host).
+struct PeelTailState {
+  alignas(128) unsigned int nloc;          // remaining vertices (local indices handed out)
+  alignas(128) unsigned long long qtail;   // claimed vertices queued (monotonic)
+  alignas(128) unsigned long long qhead;   // queue slots reserved by consumers
+  alignas(128) unsigned long long qdone;   // queued vertices processed
+  alignas(128) unsigned int claims[2];     // scan claims, by level parity
+  int mindeg[2];                           // INT_MAX - min unclaimed degree, by level parity
 };
 
 template <typename F>
@@ -593,7 +609,7 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
              int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
              uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
              int32_t* __restrict__ order, APeelShared* sh, int64_t* __restrict__ out_degeneracy,
-             unsigned poll_mask, unsigned sleep_ns, unsigned long long* trace) {
+             unsigned poll_mask, unsigned sleep_ns, unsigned long long* trace, int64_t tail_max) {
   const unsigned int G = gridDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * APEEL_THREADS + threadIdx.x;
@@ -618,6 +634,18 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
   int64_t na = n;
   int32_t k = 0x7fffffff - *(volatile int*)&sh->mindeg0, deg_max = 0;
   for (;;) {
+    // few vertices left: the remaining levels go to one thread-block cluster
+    // (k_peel_tail) -- here every level pays two grid-wide barriers
+    if (tail_max > 0 && n - (int64_t)*(volatile unsigned*)&sh->vclaim <= tail_max) {
+      if (gtid == 0) {
+        sh->tail_k = k;
+        sh->tail_degmax = deg_max;
+        sh->tail_sel = alive == alive_a ? 0 : 1;
+        sh->tail_na = (unsigned)na;
+        sh->tail = 1;
+      }
+      break;
+    }
     // ---- scan: claim every live vertex with deg <= k (degrees are stable
     // here).  A warp covers 32 * SCAN_U consecutive entries with every load
     // issued before any is used (the scan is one dependent chain, not one
@@ -805,6 +833,179 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
     k += 1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
+}
+
+// ---- the tail of the asynchronous peel on ONE thread-block cluster.  Once at
+// most PEEL_TAIL_MAX vertices remain (planted1m: the 44 k planted-clique
+// vertices and 31 sparse levels; R-MAT: the dense core and hundreds of
+// levels), each level costs the grid kernel two grid-wide barriers and a
+// few dependent L2 round trips across 148 SMs for very little work.  Here
+// the remaining vertices' degrees live in the cluster's distributed shared
+// memory (vertex j in CTA j / PEEL_TAIL_SLICE), decrements are DSMEM
+// atomics, and levels are separated by hardware cluster barriers.  Same
+// rules as k_peel_async (claim deg <= k at the level's scan, claim a vertex
+// the moment a decrement takes it from k + 1 to k, level over at quiescence,
+// k += 1 or jump to the minimum degree): a valid degeneracy order with the
+// same degeneracy.
+constexpr int PEEL_TAIL_CLUSTER = 8;
+constexpr int PEEL_TAIL_THREADS = 1024;
+#ifndef MCE_PEEL_TAIL_MAX
+#define MCE_PEEL_TAIL_MAX 65536
+#endif
+constexpr int PEEL_TAIL_MAX = MCE_PEEL_TAIL_MAX;
+constexpr int PEEL_TAIL_SLICE = PEEL_TAIL_MAX / PEEL_TAIL_CLUSTER;
+constexpr int PEEL_TAIL_BIG = 1 << 29;  // added to a claimed vertex's degree
+
+__global__ void __cluster_dims__(PEEL_TAIL_CLUSTER, 1, 1) __launch_bounds__(PEEL_TAIL_THREADS)
+k_peel_tail(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+            const int32_t* __restrict__ deg, const int32_t* alive_a, const int32_t* alive_b,
+            const uint8_t* __restrict__ removed, int32_t* __restrict__ order, APeelShared* sh,
+            PeelTailState* ts, int32_t* __restrict__ lidx, int32_t* __restrict__ gid,
+            int32_t* __restrict__ queue, int64_t* __restrict__ out_degeneracy) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  if (!*(volatile int*)&sh->tail) return;  // the grid kernel finished the peel itself
+  __shared__ int sdeg[PEEL_TAIL_SLICE];
+  const int rank = (int)cl.block_rank();
+  const int lane = threadIdx.x & 31;
+  constexpr int WPB = PEEL_TAIL_THREADS / 32;
+  constexpr int NW = PEEL_TAIL_CLUSTER * WPB;
+  const int gw = rank * WPB + (threadIdx.x >> 5);
+  const unsigned lt = (1u << lane) - 1u;
+  const int32_t* alive = sh->tail_sel ? alive_b : alive_a;
+  const unsigned na = sh->tail_na;
+  // local ids of the remaining vertices, their degrees into the owner CTA's slice
+  for (unsigned base = (unsigned)gw * 32; base < na; base += NW * 32) {
+    const unsigned i = base + lane;
+    const int32_t v = i < na ? alive[i] : -1;
+    const bool live = v >= 0 && !removed[v];
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    unsigned o = 0;
+    if (lane == 0 && m) o = atomicAdd(&ts->nloc, (unsigned)__popc(m));
+    o = __shfl_sync(0xffffffffu, o, 0);
+    if (live) {
+      const int j = (int)(o + __popc(m & lt));
+      lidx[v] = j;
+      gid[j] = v;
+      int* rd = cl.map_shared_rank(sdeg, j / PEEL_TAIL_SLICE);
+      rd[j % PEEL_TAIL_SLICE] = deg[v];
+    }
+  }
+  cl.sync();
+  const int nloc = (int)*(volatile unsigned*)&ts->nloc;
+  const int s0 = rank * PEEL_TAIL_SLICE;
+  const int s1 = min(nloc, s0 + PEEL_TAIL_SLICE);
+  int k = sh->tail_k, deg_max = sh->tail_degmax;
+  for (int level = 0;; ++level) {
+    const int p = level & 1;
+    if (rank == 0 && threadIdx.x == 0) {  // the other parity's counters, for the next level
+      ts->claims[p ^ 1] = 0;
+      ts->mindeg[p ^ 1] = 0;
+    }
+    // ---- scan of this CTA's slice (no decrements run now)
+    int md = 0x7fffffff;
+    for (int base = s0 + (threadIdx.x & ~31); base < s1; base += PEEL_TAIL_THREADS) {
+      const int j = base + lane;
+      const int d = j < s1 ? sdeg[j - s0] : PEEL_TAIL_BIG;
+      const bool take = d <= k;
+      if (d < PEEL_TAIL_BIG && !take) md = min(md, d);
+      const unsigned tm = __ballot_sync(0xffffffffu, take);
+      if (tm) {
+        unsigned pos = 0;
+        unsigned long long q = 0;
+        if (lane == 0) {
+          pos = atomicAdd(&sh->vclaim, (unsigned)__popc(tm));
+          q = atomicAdd(&ts->qtail, (unsigned long long)__popc(tm));
+          atomicAdd(&ts->claims[p], (unsigned)__popc(tm));
+        }
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (take) {
+          const int r = __popc(tm & lt);
+          sdeg[j - s0] = d + PEEL_TAIL_BIG;
+          order[pos + r] = gid[j];
+          queue[q + r] = j;
+        }
+      }
+    }
+    md = __reduce_min_sync(0xffffffffu, md);
+    if (lane == 0 && md != 0x7fffffff) atomicMax(&ts->mindeg[p], 0x7fffffff - md);
+    cl.sync();
+    const unsigned claims = *(volatile unsigned*)&ts->claims[p];
+    if (claims) deg_max = max(deg_max, k);
+    if ((int64_t)*(volatile unsigned*)&sh->vclaim >= n) break;
+    if (claims == 0) {
+      k = max(k + 1, 0x7fffffff - *(volatile int*)&ts->mindeg[p]);
+      cl.sync();  // everyone has read this parity's counters
+      continue;
+    }
+    // ---- consume the queue until quiescence: a decrement taking a vertex
+    // from k + 1 to k claims it (one DSMEM atomic decides)
+    const int kp1 = k + 1;
+    for (;;) {
+      unsigned long long h = 0;
+      if (lane == 0) h = atomicAdd(&ts->qhead, 1ull);
+      h = __shfl_sync(0xffffffffu, h, 0);
+      bool over = false;
+      int32_t item = -1;
+      for (;;) {  // slot h is written just after its producer's qtail add (-1 until then)
+        item = *(volatile int32_t*)&queue[h];
+        if (item >= 0) break;
+        // processed first, then queued: equal values mean nothing in flight
+        const unsigned long long dn = *(volatile unsigned long long*)&ts->qdone;
+        const unsigned long long qt = *(volatile unsigned long long*)&ts->qtail;
+        if (dn == qt && h >= qt) {
+          over = true;
+          break;
+        }
+        __nanosleep(32);
+      }
+      if (over) break;
+      const int32_t v = gid[item];
+      const int64_t e0 = ro[v], e1 = ro[v + 1];
+      for (int64_t base = e0; base < e1; base += 32) {
+        const int64_t e = base + lane;
+        bool claim = false;
+        int l = 0;
+        if (e < e1) {
+          const int32_t u = col[e];
+          if (!removed[u]) {
+            l = lidx[u];
+            int* rd = cl.map_shared_rank(sdeg, l / PEEL_TAIL_SLICE);
+            const int old = atomicSub(&rd[l % PEEL_TAIL_SLICE], 1);
+            if (old == kp1) {
+              atomicAdd(&rd[l % PEEL_TAIL_SLICE], PEEL_TAIL_BIG);
+              claim = true;
+            }
+          }
+        }
+        const unsigned cm = __ballot_sync(0xffffffffu, claim);
+        if (cm) {
+          unsigned pos = 0;
+          unsigned long long q = 0;
+          if (lane == 0) {
+            pos = atomicAdd(&sh->vclaim, (unsigned)__popc(cm));
+            q = atomicAdd(&ts->qtail, (unsigned long long)__popc(cm));
+          }
+          pos = __shfl_sync(0xffffffffu, pos, 0);
+          q = __shfl_sync(0xffffffffu, q, 0);
+          if (claim) {
+            const int r = __popc(cm & lt);
+            order[pos + r] = gid[l];
+            queue[q + r] = l;
+          }
+        }
+      }
+      __threadfence();  // the vertices it queued are counted before it is done
+      __syncwarp();
+      if (lane == 0) atomicAdd(&ts->qdone, 1ull);
+    }
+    cl.sync();
+    if (rank == 0 && threadIdx.x == 0) ts->qhead = *(volatile unsigned long long*)&ts->qtail;
+    k += 1;
+    cl.sync();
+  }
+  if (rank == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
 }
 
 // ids 0..n-1 (the values of the stable round sort)
@@ -1175,12 +1376,32 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
     for (int k = 0; k < APEEL_TRACE_LEVELS; ++k)  // first-quiescence slots start at ~0 (atomicMin)
       MCE_CHECK(cudaMemsetAsync(trace + 8 * k + 4, 0xff, sizeof(unsigned long long), s));
   }
+  // the last levels on one cluster (k_peel_tail); MCE_PEEL_TAIL=0 disables
+  const char* te = getenv("MCE_PEEL_TAIL");
+  const int64_t tail_max = te ? std::min<int64_t>(atoll(te), PEEL_TAIL_MAX) : PEEL_TAIL_MAX;
+  PeelTailState* ts = nullptr;
+  int32_t *lidx = nullptr, *gid = nullptr, *queue = nullptr;
+  if (tail_max > 0) {
+    if (scr.get(&ts, 1) || scr.get(&lidx, n) || scr.get(&gid, PEEL_TAIL_MAX) ||
+        scr.get(&queue, PEEL_TAIL_MAX))
+      return -1;
+    MCE_CHECK(cudaMemsetAsync(ts, 0, sizeof(PeelTailState), s));
+    MCE_CHECK(cudaMemsetAsync(queue, 0xff, sizeof(int32_t) * PEEL_TAIL_MAX, s));
+  }
   k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                    removed, order, sh, d_degeneracy,
                                                    apeel_env("MCE_APEEL_POLL", 3),
-                                                   apeel_env("MCE_APEEL_SLEEP", 32), trace);
+                                                   apeel_env("MCE_APEEL_SLEEP", 32), trace,
+                                                   tail_max);
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
+  if (tail_max > 0) {
+    k_peel_tail<<<PEEL_TAIL_CLUSTER, PEEL_TAIL_THREADS, 0, s>>>(
+        g->ro, g->col, n, deg, alive, alive2, removed, order, sh, ts, lidx, gid, queue,
+        d_degeneracy);
+    mce_count_launch();
+    MCE_CHECK(cudaGetLastError());
+  }
   if (trace) {
     std::vector<unsigned long long> h(trace_words);
     MCE_CHECK(cudaMemcpyAsync(h.data(), trace, sizeof(unsigned long long) * trace_words,

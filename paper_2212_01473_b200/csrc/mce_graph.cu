@@ -835,11 +835,11 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
 }
 
-// ---- the tail of the asynchronous peel on ONE thread-block cluster.  Once at
-// most PEEL_TAIL_MAX vertices remain (planted1m: the 44 k planted-clique
-// vertices and 31 sparse levels; R-MAT: the dense core and hundreds of
-// levels), each level costs the grid kernel two grid-wide barriers and a
-// few dependent L2 round trips across 148 SMs for very little work.  Here
+// ---- the asynchronous peel on ONE thread-block cluster, for the last levels
+// (at most PEEL_TAIL_MAX vertices left) -- by default only small graphs
+// (n <= PEEL_TAIL_SMALL_N), which it peels whole: a level costs the grid
+// kernel two grid-wide barriers and a few dependent L2 round trips across
+// 148 SMs for very little work.  Here
 // the remaining vertices' degrees live in the cluster's distributed shared
 // memory (vertex j in CTA j / PEEL_TAIL_SLICE), decrements are DSMEM
 // atomics, and levels are separated by hardware cluster barriers.  Same
@@ -855,6 +855,7 @@ constexpr int PEEL_TAIL_THREADS = 1024;
 constexpr int PEEL_TAIL_MAX = MCE_PEEL_TAIL_MAX;
 constexpr int PEEL_TAIL_SLICE = PEEL_TAIL_MAX / PEEL_TAIL_CLUSTER;
 constexpr int PEEL_TAIL_BIG = 1 << 29;  // added to a claimed vertex's degree
+constexpr int64_t PEEL_TAIL_SMALL_N = 8192;  // graphs this small peel on the cluster only
 
 __global__ void __cluster_dims__(PEEL_TAIL_CLUSTER, 1, 1) __launch_bounds__(PEEL_TAIL_THREADS)
 k_peel_tail(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
@@ -1376,9 +1377,15 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
     for (int k = 0; k < APEEL_TRACE_LEVELS; ++k)  // first-quiescence slots start at ~0 (atomicMin)
       MCE_CHECK(cudaMemsetAsync(trace + 8 * k + 4, 0xff, sizeof(unsigned long long), s));
   }
-  // the last levels on one cluster (k_peel_tail); MCE_PEEL_TAIL=0 disables
+  // Small graphs peel entirely on one cluster (k_peel_tail).  A larger graph's
+  // last levels could too (MCE_PEEL_TAIL=<remaining vertices>), but measured
+  // slower there: one warp per claimed vertex serialises the hubs of an
+  // R-MAT core (rmat20 8.8 -> 11.9 ms at 4096) and 8 SMs cannot absorb a
+  // planted1m level (1.88 -> 2.62 ms at 65536) -- the grid kernel's 32-edge
+  // chunk tasks spread both over the whole GPU.
   const char* te = getenv("MCE_PEEL_TAIL");
-  const int64_t tail_max = te ? std::min<int64_t>(atoll(te), PEEL_TAIL_MAX) : PEEL_TAIL_MAX;
+  const int64_t tail_max = te ? std::min<int64_t>(atoll(te), PEEL_TAIL_MAX)
+                              : (n <= PEEL_TAIL_SMALL_N ? n : 0);
   PeelTailState* ts = nullptr;
   int32_t *lidx = nullptr, *gid = nullptr, *queue = nullptr;
   if (tail_max > 0) {

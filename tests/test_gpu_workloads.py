@@ -214,14 +214,20 @@ def _later_counts(ro, ci, pos):
     return np.bincount(src[later], minlength=len(ro) - 1)
 
 
-@pytest.mark.parametrize("name", ["er2k", "ba200k", "planted1m"])
-def test_async_peel_is_a_degeneracy_order(name):
+@pytest.mark.parametrize("name,tail", [("er2k", None), ("ba200k", None), ("planted1m", None),
+                                       ("ba200k", "65536"), ("planted1m", "65536"),
+                                       ("planted1m", "1")])
+def test_async_peel_is_a_degeneracy_order(name, tail, monkeypatch):
     """method="async" (no rounds inside a level): a permutation whose every
     vertex has at most d later neighbours, d the reference's degeneracy --
     checked on repeated runs, since its tie-breaks are data-dependent -- and
-    the same clique set as the other orders."""
+    the same clique set as the other orders.  ``tail`` forces the hand-over
+    of the last levels to the cluster kernel (k_peel_tail) at that many
+    remaining vertices (er2k runs on it whole by default)."""
     from paper_2212_01473_b200 import degeneracy_order
 
+    if tail is not None:
+        monkeypatch.setenv("MCE_PEEL_TAIL", tail)
     edges, n = generate.workload_edges(name)
     g = from_edges(edges, n)
     ro, ci = g.row_offsets, g.col_indices

@@ -723,7 +723,7 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       trace[8 * k + 0] = t;
       trace[8 * k + 1] = claims;
-      trace[8 * k + 2] = na;
+      trace[8 * k + 2] = ~0ull;  // first chunk taken (atomicMin below)
     }
     const unsigned vc = *(volatile unsigned*)&sh->vclaim;
     const int32_t mn = *(volatile int*)&sh->mindeg;
@@ -786,6 +786,11 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
           if (sleep_ns) __nanosleep(sleep_ns);
         }
         if (over) break;
+        if (trace && lane == 0 && got == 0 && k < APEEL_TRACE_LEVELS) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          atomicMin(&trace[8 * k + 2], t);
+        }
         // c chunks: lane l takes edge l of each; c decrements in flight per lane
         int32_t u[APEEL_BATCH];
 #pragma unroll
@@ -1417,12 +1422,12 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
     if (FILE* f = fopen(trace_path, "a")) {
       const unsigned long long t0 = h[8 * APEEL_TRACE_LEVELS];
       auto us = [&](unsigned long long t) { return (t && t != ~0ull) ? (double)(t - t0) / 1e3 : -1.0; };
-      fprintf(f, "# n=%lld grid=%lld: k scan_end_us claims alive first_quiesce_us last_quiesce_us "
-                 "last_work_us chunks level_end_us\n", (long long)n, (long long)grid);
+      fprintf(f, "# n=%lld grid=%lld: k scan_end_us claims first_work_us first_quiesce_us "
+                 "last_quiesce_us last_work_us chunks level_end_us\n", (long long)n, (long long)grid);
       for (int k = 0; k < APEEL_TRACE_LEVELS; ++k)
         if (h[8 * k])
-          fprintf(f, "%d %.1f %llu %llu %.1f %.1f %.1f %llu %.1f\n", k, us(h[8 * k]), h[8 * k + 1],
-                  h[8 * k + 2], us(h[8 * k + 4]), us(h[8 * k + 5]), us(h[8 * k + 6]), h[8 * k + 7],
+          fprintf(f, "%d %.1f %llu %.1f %.1f %.1f %.1f %llu %.1f\n", k, us(h[8 * k]), h[8 * k + 1],
+                  us(h[8 * k + 2]), us(h[8 * k + 4]), us(h[8 * k + 5]), us(h[8 * k + 6]), h[8 * k + 7],
                   us(h[8 * k + 3]));
       fclose(f);
     }

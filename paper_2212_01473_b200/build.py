@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmce_b200.so")
 SOURCES = ["mce_graph.cu", "mce_enum.cu", "mce_synth.cu", "mce_text.cu"]
-HEADERS = ["mce_common.cuh"]
+HEADERS = ["mce_common.cuh", "mce_tiny.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -2164,7 +2164,7 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
 
 // the lane-per-root kernel over the |P| <= 32 roots, timed by its own event pair
 int launch_tiny(bool full, TinyArgs ta, cudaStream_t s, cudaEvent_t* ev, int64_t* launches,
-                int64_t* workers_used) {
+                int64_t* workers_used, Scratch& scr) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2194,6 +2194,7 @@ int launch_tiny(bool full, TinyArgs ta, cudaStream_t s, cudaEvent_t* ev, int64_t
   else ta.max_warps = (int)(g * TINY_WARPS);
   const int grid = (int)g;
   *workers_used = std::max<int64_t>(*workers_used, ta.max_warps);
+  if (scr.get(&ta.spill, (size_t)grid * TINY_THREADS * TINY_SPILL * 8)) return -1;
   MCE_CHECK(cudaEventRecord(ev[0], s));
   kern<<<grid, TINY_THREADS, smem, s>>>(ta);
   mce_count_launch();
@@ -2351,6 +2352,7 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     pin_cap[ev_dev] = zwords;
   }
   unsigned long long* pin = pin_buf[ev_dev];
+  unsigned long long* tiny_reasons = nullptr;  // diagnostics (MCE_TRACE)
   tr.mark("vhash+events");
   if (count > 0) {
     uint32_t *keys = nullptr, *keys2 = nullptr;
@@ -2525,7 +2527,16 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
         ta.max_warps = cfg->workers > 0 ? cfg->workers : 0;
         ta.no_pivot = cfg->no_pivot;
         ta.timing = cfg->timing;
-        if (launch_tiny(full, ta, s, &events[2 * nev++], &launches, &workers_used)) {
+        ta.reasons = nullptr;
+        if (tr.on) {
+          if (get(&ta.reasons, 8)) {
+            cleanup();
+            return -1;
+          }
+          MCE_CHECK(cudaMemsetAsync(ta.reasons, 0, 8 * sizeof(unsigned long long), s));
+          tiny_reasons = ta.reasons;
+        }
+        if (launch_tiny(full, ta, s, &events[2 * nev++], &launches, &workers_used, scr)) {
           cleanup();
           return -1;
         }
@@ -2610,9 +2621,14 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
   tr.mark("results queued");
   MCE_CHECK(cudaStreamSynchronize(s));
   tr.mark("results synced");
-  if (tr.on)
-    fprintf(stderr, "[mce_trace] k_tiny handed back %llu roots to the warp kernel\n",
-            pin[ZB_CLS + MAXP_SLOT + 1 + 3 + 1]);
+  if (tr.on) {
+    unsigned long long rs[8] = {0};
+    if (tiny_reasons)
+      cudaMemcpy(rs, tiny_reasons, sizeof(rs), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[mce_trace] k_tiny handed back %llu roots to the warp kernel (heavy-X %llu, "
+            "|P|>32 %llu, |X|>%d %llu, row pool %llu, dense %llu)\n",
+            pin[ZB_CLS + MAXP_SLOT + 1 + 3 + 1], rs[0], rs[1], TINY_XT, rs[2], rs[3], rs[4]);
+  }
   unsigned long long h_acc[8];
   memcpy(h_acc, pin, sizeof(h_acc));
   memcpy(out->hist, pin + 8, sizeof(int64_t) * HIST_MAX);

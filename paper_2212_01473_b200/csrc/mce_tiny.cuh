@@ -50,7 +50,14 @@ constexpr int tiny_max_clique(int e) {
   while ((c + 1) * c / 2 <= e) ++c;
   return c;
 }
-constexpr int TINY_DEPTH = tiny_max_clique(TINY_E_MAX) + 1;
+constexpr int TINY_DEPTH = tiny_max_clique(TINY_E_MAX) + 1;  // local frames
+constexpr int TINY_SPILL = 33 - TINY_DEPTH;  // global frames (a pushed level holds a P member)
+// a root denser than TINY_E_MAX edges stays here when its P misses at most
+// TINY_M_MAX edges (a near-clique: few maximal cliques, a short tree)
+#ifndef MCE_TINY_M_MAX
+#define MCE_TINY_M_MAX 16
+#endif
+constexpr int TINY_M_MAX = MCE_TINY_M_MAX;
 constexpr int TINY_WARP_WORDS = TINY_SLICE + TINY_POOL + 64;  // + 32 bloom words (64-bit)
 constexpr int TINY_SMEM_WORDS = HIST_SMEM + TINY_WARP_WORDS * TINY_WARPS;
 
@@ -71,6 +78,8 @@ struct TinyArgs {
   int max_warps;                     // workers requested (warps >= this stay idle)
   int no_pivot;                      // basic Bron-Kerbosch: branch on all of P
   int timing;                        // SM cycles by category into w_metrics
+  unsigned long long* reasons;       // diagnostics (MCE_TRACE): hand-backs by cause
+  uint32_t* spill;                   // DFS frames past TINY_DEPTH: TINY_SPILL x 8 words per thread
 };
 
 __device__ __forceinline__ void tiny_hist_add(unsigned* s_hist, unsigned long long* g_hist, int size) {
@@ -102,10 +111,14 @@ __device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, c
   uint32_t P = np == 32 ? ~0u : ((1u << np) - 1u), XP = 0, BR = 0, NL = 0;
   int rlen = 1, depth = 0;
   nodes++;
-  // depth <= (max clique size in P) - 1 <= TINY_DEPTH - 1 under TINY_E_MAX edges
+  // Frames are pushed only for levels with non-leaf branches left (a level
+  // whose last branch is being visited is never returned to: a tail call),
+  // so a clique-like P needs next to none.  The first TINY_DEPTH frames live
+  // in local memory (L1); deeper ones in this thread's global spill slots.
   uint32_t fP[TINY_DEPTH], fXP[TINY_DEPTH], fBR[TINY_DEPTH], fNL[TINY_DEPTH];
-  int flive[TINY_DEPTH];
+  int flr[TINY_DEPTH];  // live | rlen << 16
   uint64_t fhs[TINY_DEPTH];
+  uint32_t* spill = a.spill + ((size_t)blockIdx.x * TINY_THREADS + threadIdx.x) * TINY_SPILL * 8;
   bool fresh = true;
   for (;;) {
     if (fresh) {
@@ -159,13 +172,25 @@ __device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, c
     if (NL == 0) {
       if (depth == 0) break;
       depth--;
-      rlen--;
-      P = fP[depth];
-      XP = fXP[depth];
-      BR = fBR[depth];
-      NL = fNL[depth];
-      live = flive[depth];
-      hs = fhs[depth];
+      int lr;
+      if (depth < TINY_DEPTH) {
+        P = fP[depth];
+        XP = fXP[depth];
+        BR = fBR[depth];
+        NL = fNL[depth];
+        lr = flr[depth];
+        hs = fhs[depth];
+      } else {
+        const uint32_t* f = spill + (depth - TINY_DEPTH) * 8;
+        P = f[0];
+        XP = f[1];
+        BR = f[2];
+        NL = f[3];
+        lr = (int)f[4];
+        hs = (uint64_t)f[5] | ((uint64_t)f[6] << 32);
+      }
+      live = lr & 0xffff;
+      rlen = lr >> 16;
       continue;
     }
     // move v and the (leaf) branches before it from P to X_P
@@ -188,13 +213,26 @@ __device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, c
         xm[kept++] = r;
       }
     }
-    fP[depth] = P;
-    fXP[depth] = XP;
-    fBR[depth] = BR;
-    fNL[depth] = NL;
-    flive[depth] = live;
-    fhs[depth] = hs;
-    depth++;
+    if (NL) {  // this level has branches left: come back to it
+      if (depth < TINY_DEPTH) {
+        fP[depth] = P;
+        fXP[depth] = XP;
+        fBR[depth] = BR;
+        fNL[depth] = NL;
+        flr[depth] = live | (rlen << 16);
+        fhs[depth] = hs;
+      } else {
+        uint32_t* f = spill + (depth - TINY_DEPTH) * 8;
+        f[0] = P;
+        f[1] = XP;
+        f[2] = BR;
+        f[3] = NL;
+        f[4] = (uint32_t)(live | (rlen << 16));
+        f[5] = (uint32_t)hs;
+        f[6] = (uint32_t)(hs >> 32);
+      }
+      depth++;
+    }
     live = kept;
     XP &= rv;
     P &= rv;
@@ -206,7 +244,11 @@ __device__ __forceinline__ void tiny_dfs(const TinyArgs& a, const int32_t* pl, c
 }
 
 template <bool PIVOT_XX>
-__global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
+// 80 registers: three 256-thread CTAs per SM (allocation is in 8-register steps)
+#ifndef MCE_TINY_MAXREG
+#define MCE_TINY_MAXREG 80
+#endif
+__global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
   extern __shared__ __align__(16) uint32_t tsm[];
   unsigned* s_hist = tsm;
   const int warp = threadIdx.x >> 5;
@@ -251,6 +293,8 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
       nx = (int)(s0 - xb0);
     }
     bool ok = valid && (renc >> ROOT_ID_BITS) == 0 && np <= 32 && nx <= TINY_XT;
+    if (a.reasons && valid && !ok)
+      atomicAdd(&a.reasons[(renc >> ROOT_ID_BITS) ? 0 : (np > 32 ? 1 : 2)], 1ull);
     if (!ok) np = nx = 0;
     // root r's rows and X rows: np + nx words of the warp's pool at its
     // prefix offset (roots past the pool's end go to the warp kernel)
@@ -263,6 +307,7 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
     }
     if (__any_sync(FULLMASK, incl > TINY_POOL)) {  // the suffix past the pool's end
       if (incl > TINY_POOL) {
+        if (a.reasons && ok) atomicAdd(&a.reasons[3], 1ull);
         ok = false;
         np = nx = cnt = 0;
       }
@@ -385,7 +430,8 @@ __global__ void __launch_bounds__(TINY_THREADS, 2) k_tiny(TinyArgs a) {
     if (ok) {
       int e2 = 0;
       for (int k = 0; k < np; ++k) e2 += __popc(myrow[k]);
-      if (e2 > 2 * TINY_E_MAX) {
+      if (e2 > 2 * TINY_E_MAX && np * (np - 1) - e2 > 2 * TINY_M_MAX) {
+        if (a.reasons) atomicAdd(&a.reasons[4], 1ull);
         ok = false;
       } else {
         // X members with no neighbour in P never matter (see init_tokens)

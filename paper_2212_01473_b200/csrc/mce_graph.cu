@@ -508,6 +508,7 @@ struct APeelShared {
   int tail;
   int tail_k, tail_degmax, tail_sel;
   unsigned int tail_na;
+  alignas(128) unsigned int scans_done;  // k_peel_async1: warps past this level's scan
 };
 
 // The tail kernel's own counters (zeroed by the host).
@@ -836,6 +837,190 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
       trace[8 * k + 3] = t;
     }
     k += 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
+}
+
+// ---- one grid barrier per level (k_peel_async1, the default): the level's
+// scan runs concurrently with the consumers of the chunks it produces, and
+// quiescence additionally waits for every warp's scan (a counter bumped
+// after its claims are counted).  A scan and a decrement may then want the
+// same vertex (its degree dropped to k while the scan looked at it): a
+// claim is a test-and-set on the `rbits` bitmap, so exactly one wins.  The
+// rules are k_peel_async's otherwise -- the same valid degeneracy order
+// family and degeneracy -- with one barrier and no scan -> consumer hand-off
+// per level instead of two barriers.
+__global__ void __launch_bounds__(APEEL_THREADS)
+k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+              int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
+              uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
+              unsigned* __restrict__ rbits, int32_t* __restrict__ order, APeelShared* sh,
+              int64_t* __restrict__ out_degeneracy, unsigned poll_mask, unsigned sleep_ns,
+              int64_t tail_max) {
+  const unsigned int G = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * APEEL_THREADS + threadIdx.x;
+  const int64_t gstride = (int64_t)G * APEEL_THREADS;
+  const unsigned total_warps = G * (APEEL_THREADS / 32);
+  auto nothing = [] {};
+  int dmin = 0x7fffffff;
+  for (int64_t v = gtid; v < n; v += gstride) {
+    const int32_t d0 = (int32_t)(ro[v + 1] - ro[v]);
+    deg[v] = d0;
+    dmin = min(dmin, (int)d0);
+    alive_a[v] = (int32_t)v;
+    removed[v] = 0;
+  }
+  for (int64_t w = gtid; w < (n + 31) / 32; w += gstride) rbits[w] = 0;
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0 && dmin != 0x7fffffff) atomicMax(&sh->mindeg0, 0x7fffffff - dmin);
+  if (gtid == 0) sh->mindeg = 0x7fffffff;  // the rest of *sh is zeroed by the host
+  agrid_barrier(sh, G, nothing);
+  int32_t* alive = alive_a;
+  int32_t* alive2 = alive_b;
+  int64_t na = n;
+  int32_t k = 0x7fffffff - *(volatile int*)&sh->mindeg0, deg_max = 0;
+  // test-and-set claim of v: true for exactly one caller
+  auto claim = [&](int32_t v) {
+    const unsigned bit = 1u << (v & 31);
+    return !(atomicOr(&rbits[v >> 5], bit) & bit);
+  };
+  for (;;) {
+    const unsigned vc0 = *(volatile unsigned*)&sh->vclaim;
+    if (tail_max > 0 && n - (int64_t)vc0 <= tail_max) {  // see k_peel_async
+      if (gtid == 0) {
+        sh->tail_k = k;
+        sh->tail_degmax = deg_max;
+        sh->tail_sel = alive == alive_a ? 0 : 1;
+        sh->tail_na = (unsigned)na;
+        sh->tail = 1;
+      }
+      break;
+    }
+    // ---- scan (consumers may already be decrementing)
+    constexpr int SCAN_U = 8;
+    for (int64_t base = (gtid - lane) * SCAN_U; base < na; base += gstride * SCAN_U) {
+      int32_t v[SCAN_U], d[SCAN_U];
+      unsigned rb[SCAN_U];
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        const int64_t i = base + u * 32 + lane;
+        v[u] = i < na ? __ldcg(&alive[i]) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        rb[u] = v[u] >= 0 ? __ldcg(&rbits[v[u] >> 5]) : ~0u;
+        d[u] = v[u] >= 0 ? __ldcg(&deg[v[u]]) : 0x7fffffff;
+      }
+      int64_t e0[SCAN_U], e1[SCAN_U];
+      int nkeep = 0, md = 0x7fffffff;
+      unsigned km[SCAN_U], tmask = 0;
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        const bool live = v[u] >= 0 && !((rb[u] >> (v[u] & 31)) & 1u);
+        const bool take = live && d[u] <= k && claim(v[u]);
+        const bool keep = live && d[u] > k;
+        km[u] = __ballot_sync(0xffffffffu, keep);
+        nkeep += __popc(km[u]);
+        if (keep) md = min(md, (int)d[u]);
+        if (take) tmask |= 1u << u;
+      }
+#pragma unroll
+      for (int u = 0; u < SCAN_U; ++u) {
+        const bool t = (tmask >> u) & 1u;
+        e0[u] = t ? ro[v[u]] : 0;
+        e1[u] = t ? ro[v[u] + 1] : 0;
+      }
+      if (nkeep) {
+        unsigned o = 0;
+        if (lane == 0) o = atomicAdd(&sh->acount, (unsigned)nkeep);
+        o = __shfl_sync(0xffffffffu, o, 0);
+        const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+        for (int u = 0; u < SCAN_U; ++u) {
+          if ((km[u] >> lane) & 1u) alive2[o + __popc(km[u] & lt)] = v[u];
+          o += __popc(km[u]);
+        }
+        md = __reduce_min_sync(0xffffffffu, md);
+        if (lane == 0) atomicMin(&sh->mindeg, md);
+      }
+      if (__any_sync(0xffffffffu, tmask != 0))
+        apeel_claim<SCAN_U>(v, e0, e1, tmask, 0u, sh, tasks, order, removed, lane);
+    }
+    __threadfence();  // this warp's claims are counted before its scan is
+    if (lane == 0) atomicAdd(&sh->scans_done, 1u);
+    // ---- consume chunks until every scan is done and nothing is in flight
+    const int32_t kp1 = k + 1;
+    bool over = false;
+    while (!over) {
+      unsigned long long h = 0;
+      if (lane == 0) h = atomicAdd(&sh->head, (unsigned long long)APEEL_BATCH);
+      h = __shfl_sync(0xffffffffu, h, 0);
+      int got = 0;
+      while (got < APEEL_BATCH) {
+        uint64_t dsc = TASK_EMPTY;
+        int c = 0;
+        for (unsigned polls = 0;; ++polls) {
+          dsc = lane < APEEL_BATCH - got ? __ldcv(&tasks[h + got + lane]) : TASK_EMPTY;
+          const unsigned av = __ballot_sync(0xffffffffu, dsc != TASK_EMPTY);
+          c = __ffs(~av) - 1;
+          if (c > 0) break;
+          if ((polls & poll_mask) == poll_mask) {
+            // scans first, then done, then claimed (all monotonic in a level)
+            const unsigned sd = __ldcv(&sh->scans_done);
+            const unsigned long long dn = __ldcv(&sh->tdone);
+            const unsigned long long cl = __ldcv(&sh->tclaim);
+            if ((sd == total_warps && cl == dn && h + got >= cl) ||
+                __ldcv(&sh->vclaim) >= (unsigned)n) {
+              over = true;
+              break;
+            }
+          }
+          if (sleep_ns) __nanosleep(sleep_ns);
+        }
+        if (over) break;
+        int32_t u[APEEL_BATCH];
+#pragma unroll
+        for (int t = 0; t < APEEL_BATCH; ++t) {
+          const uint64_t dt = __shfl_sync(0xffffffffu, dsc, t);
+          u[t] = -1;
+          if (t < c && lane < (int)(dt & 63)) u[t] = col[(int64_t)(dt >> 6) + lane];
+        }
+        int64_t r0[APEEL_BATCH], r1[APEEL_BATCH];
+        int old_deg[APEEL_BATCH];
+#pragma unroll
+        for (int t = 0; t < APEEL_BATCH; ++t) {
+          r0[t] = u[t] >= 0 ? __ldg(&ro[u[t]]) : 0;
+          r1[t] = u[t] >= 0 ? __ldg(&ro[u[t] + 1]) : 0;
+          old_deg[t] = u[t] >= 0 ? atomicSub(&deg[u[t]], 1) : 0;
+        }
+        unsigned cm = 0;
+#pragma unroll
+        for (int t = 0; t < APEEL_BATCH; ++t)
+          if (u[t] >= 0 && old_deg[t] == kp1 && claim(u[t])) cm |= 1u << t;
+        apeel_claim<APEEL_BATCH>(u, r0, r1, cm, (unsigned)c, sh, tasks, order, removed, lane);
+        got += c;
+      }
+    }
+    // the level's results are final here (every scan done, nothing in flight)
+    const unsigned vc = *(volatile unsigned*)&sh->vclaim;
+    const int32_t mn = *(volatile int*)&sh->mindeg;
+    na = *(volatile unsigned*)&sh->acount;
+    {
+      int32_t* t = alive;
+      alive = alive2;
+      alive2 = t;
+    }
+    const bool claimed = vc > vc0;
+    if (claimed) deg_max = max(deg_max, k);
+    agrid_barrier(sh, G, [sh] {
+      sh->head = sh->tclaim;
+      sh->scans_done = 0;
+      sh->acount = 0;
+      sh->mindeg = 0x7fffffff;
+    });
+    if ((int64_t)vc >= n) break;
+    k = claimed ? k + 1 : max(k + 1, mn);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
 }
@@ -1350,8 +1535,12 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static int per_sm = -1;
-  if (per_sm < 0)
-    MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_async, APEEL_THREADS, 0));
+  if (per_sm < 0) {  // (both variants: the smaller residency bounds the grid)
+    int a = 0, b = 0;
+    MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_peel_async, APEEL_THREADS, 0));
+    MCE_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_peel_async1, APEEL_THREADS, 0));
+    per_sm = std::min(a, b);
+  }
   if (per_sm < 1) {
     mce_set_error("async peel kernel does not fit on an SM");
     return -3;
@@ -1400,11 +1589,23 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
     MCE_CHECK(cudaMemsetAsync(ts, 0, sizeof(PeelTailState), s));
     MCE_CHECK(cudaMemsetAsync(queue, 0xff, sizeof(int32_t) * PEEL_TAIL_MAX, s));
   }
-  k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
-                                                   removed, order, sh, d_degeneracy,
-                                                   apeel_env("MCE_APEEL_POLL", 3),
-                                                   apeel_env("MCE_APEEL_SLEEP", 32), trace,
-                                                   tail_max);
+  // one barrier per level (k_peel_async1) unless the per-level trace is on
+  // or MCE_PEEL_MERGED=0 (diagnostics)
+  const bool merged = !trace && apeel_env("MCE_PEEL_MERGED", 1) != 0;
+  if (merged) {
+    unsigned* rbits = nullptr;
+    if (scr.get(&rbits, (n + 31) / 32)) return -1;
+    k_peel_async1<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
+                                                      removed, rbits, order, sh, d_degeneracy,
+                                                      apeel_env("MCE_APEEL_POLL", 3),
+                                                      apeel_env("MCE_APEEL_SLEEP", 32), tail_max);
+  } else {
+    k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
+                                                     removed, order, sh, d_degeneracy,
+                                                     apeel_env("MCE_APEEL_POLL", 3),
+                                                     apeel_env("MCE_APEEL_SLEEP", 32), trace,
+                                                     tail_max);
+  }
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
   if (tail_max > 0) {

@@ -1678,9 +1678,25 @@ struct Worker {
 #ifndef MCE_MINB_SMALL
 #define MCE_MINB_SMALL 4
 #endif
+// The wide classes are latency-bound with few warps per SM (register-limited
+// at ~210 registers): capping them buys residency.  Measured on rmat20's
+// core: the W = 32 class on one dense root 20.8 s (2 CTAs of 4 warps per SM)
+// -> 15.5 s (3 CTAs, 167 registers); W = 8 / 16 chunk 935 -> 888 ms.
+#ifndef MCE_MINB_W8
+#define MCE_MINB_W8 4
+#endif
+#ifndef MCE_MINB_W16
+#define MCE_MINB_W16 6
+#endif
+#ifndef MCE_MINB_W32
+#define MCE_MINB_W32 3
+#endif
 template <int W>
 struct MinBlocks {
-  static constexpr int value = W <= 4 ? MCE_MINB_SMALL : 1;
+  static constexpr int value = W <= 4 ? MCE_MINB_SMALL
+                               : W == 8 ? MCE_MINB_W8
+                               : W == 16 ? MCE_MINB_W16
+                               : W == 32 ? MCE_MINB_W32 : 1;
 };
 
 template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
@@ -1706,7 +1722,9 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
     int stripe = wid % ROOT_STRIPES;
     bool phase1 = true;
     const long long t_start = clock64();
-    if (a.phase_ns && lane == 0) atomicMax(&a.phase_ns[0], ~gtimer());
+    // launch phase times with few same-address atomics: the start by one thread,
+    // the first root-list miss and the last end only while they can still move
+    if (a.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&a.phase_ns[0], ~gtimer());
     // one traverse() call site (inlined once): phase 1 claims independent
     // subtrees (scheduler.py:253-273), phase 2 parks on the worker list and
     // receives donated branches
@@ -1720,7 +1738,8 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
         wk.toc(T_WLIST, t0);
         if (idx < 0) {
           phase1 = false;
-          if (a.phase_ns && lane == 0) atomicMax(&a.phase_ns[1], ~gtimer());
+          if (a.phase_ns && lane == 0 && !*(volatile unsigned long long*)&a.phase_ns[1])
+            atomicMax(&a.phase_ns[1], ~gtimer());
           if (!a.worker_list_on) break;
           continue;
         }
@@ -1754,7 +1773,10 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
       m[2] += wk.don_made;
       m[3] += wk.don_recv;
       if (a.timing) m[T_TOTAL] += clock64() - t_start;
-      if (a.phase_ns) atomicMax(&a.phase_ns[2], gtimer());
+      if (a.phase_ns) {
+        const unsigned long long t = gtimer();
+        if (t > *(volatile unsigned long long*)&a.phase_ns[2]) atomicMax(&a.phase_ns[2], t);
+      }
     }
   }
   __syncthreads();

@@ -260,7 +260,7 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
   __syncthreads();
   const int gw = (int)((blockIdx.x * TINY_THREADS + threadIdx.x) >> 5);
   const int32_t* __restrict__ col = a.col;
-  if (a.phase_ns && lane == 0) atomicMax(&a.phase_ns[0], ~gtimer());
+  if (a.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&a.phase_ns[0], ~gtimer());
   const long long t_start = clock64();
   long long t_build = 0, t_dfs = 0, t_claim = 0;
   const unsigned lt = (1u << lane) - 1u;
@@ -460,8 +460,9 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
   }
   if (a.phase_ns && lane == 0 && gw < a.max_warps) {
     const unsigned long long t = gtimer();
-    atomicMax(&a.phase_ns[1], ~t);  // this warp found the root list exhausted
-    atomicMax(&a.phase_ns[2], t);
+    if (!*(volatile unsigned long long*)&a.phase_ns[1])
+      atomicMax(&a.phase_ns[1], ~t);  // the first warp to find the root list exhausted
+    if (t > *(volatile unsigned long long*)&a.phase_ns[2]) atomicMax(&a.phase_ns[2], t);
   }
   // warp totals (64-bit shuffles), one set of atomics per warp
   unsigned long long c = cliques, h = hash, nd = nodes, mx = max_size;

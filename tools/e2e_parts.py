@@ -8,7 +8,7 @@ from paper_2212_01473_b200 import RunConfig, from_edges, generate, preprocess, r
 
 name = sys.argv[1] if len(sys.argv) > 1 else "ba200k"
 edges, n = generate.workload_edges(name)
-host = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory()
+host = torch.from_numpy(np.ascontiguousarray(edges, dtype=np.int32)).pin_memory()  # as bench.py
 hn = host.numpy()
 dev = torch.empty_like(host, device="cuda")
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -24,5 +24,5 @@ for _ in range(20):
     t_copy.append(ev[0].elapsed_time(ev[1])); t_fe.append(ev[2].elapsed_time(ev[3]))
     ev[0].record(); g2, _, st = preprocess(g); r = run(g2, st, RunConfig()); ev[1].record()
     torch.cuda.synchronize(); t_rest.append(ev[0].elapsed_time(ev[1]))
-print(f"{name}: H2D {host.numel()*8/1e6:.1f} MB {np.median(t_copy):.3f} ms ({host.numel()*8/np.median(t_copy)/1e6:.1f} GB/s); "
+print(f"{name}: H2D {host.numel()*4/1e6:.1f} MB {np.median(t_copy):.3f} ms ({host.numel()*4/np.median(t_copy)/1e6:.1f} GB/s); "
       f"from_edges {np.median(t_fe):.3f} ms; preprocess+run {np.median(t_rest):.3f} ms")

@@ -175,21 +175,7 @@ int bits_for(int64_t n) {
 
 // ---------------------------------------------------------------- kernels
 
-// (lo << b | hi) keys; self-loops become ~0 (dropped); ids outside [0, n)
-// raise `bad` (reference: ValueError, graph.py:103-129)
-__global__ void k_edge_keys(const int64_t* __restrict__ edges, int64_t m, int b, int64_t n,
-                            uint64_t* __restrict__ keys, int* __restrict__ bad) {
-  bool oob = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = edges[2 * i], c = edges[2 * i + 1];
-    oob |= (a < 0) | (c < 0) | (a >= n) | (c >= n);
-    int64_t lo = a < c ? a : c, hi = a < c ? c : a;
-    keys[i] = (lo == hi) ? ~0ull : (((uint64_t)lo << b) | (uint64_t)hi);
-  }
-  if (__syncthreads_or(oob) && threadIdx.x == 0) atomicExch(bad, 1);
-}
-
+// ids outside [0, n) raise `bad` (reference: ValueError, graph.py:103-129)
 // both directed keys of every input pair; loops -> all-ones (dropped later).
 // T = int64_t (the reference's edge array) or int32_t (half the ingress bytes)
 template <typename T>
@@ -212,22 +198,6 @@ __global__ void k_last_is_loop(const uint64_t* __restrict__ uniq, int64_t* cnt, 
   const int64_t u = cnt[0];
   const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
   cnt[2] = (u > 0 && (uniq[u - 1] & mask) == mask) ? 1 : 0;
-}
-
-struct NotAllOnes {
-  __host__ __device__ bool operator()(const uint64_t& k) const { return k != ~0ull; }
-};
-
-__global__ void k_expand_directed(const uint64_t* __restrict__ und, int64_t m, int b,
-                                  uint64_t* __restrict__ out) {
-  const uint64_t mask = (1ull << b) - 1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = und[i];
-    uint64_t lo = k >> b, hi = k & mask;
-    out[2 * i] = k;
-    out[2 * i + 1] = (hi << b) | lo;
-  }
 }
 
 // keys sorted by (src, dst): emit col and row offsets
@@ -1445,6 +1415,276 @@ int sort_keys(uint64_t** keys, int64_t count, int end_bit, cudaStream_t s) {
   return 0;
 }
 
+// ---- row-wise canonicalisation (from_edges, graph.py:103-129): count each
+// vertex's endpoints, scatter the directed entries into their rows, then
+// sort + deduplicate every row where it lies (registers for rows <= 256,
+// one CTA in shared memory up to LONGROW_MAX) and compact.  Instead of one
+// radix sort of 2E 64-bit (u, v) keys over 2 log n bits (5 full passes on
+// planted1m), each entry moves about twice.
+template <typename T>
+__global__ void k_count_endpoints(const T* __restrict__ edges, int64_t m, int64_t n,
+                                  int32_t* __restrict__ cnt, int* __restrict__ bad) {
+  bool oob = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = edges[2 * i], c = edges[2 * i + 1];
+    const bool o = (a < 0) | (c < 0) | (a >= n) | (c >= n);
+    oob |= o;
+    if (!o && a != c) {
+      atomicAdd(&cnt[a], 1);
+      atomicAdd(&cnt[c], 1);
+    }
+  }
+  if (__syncthreads_or(oob) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+template <typename T>
+__global__ void k_scatter_endpoints(const T* __restrict__ edges, int64_t m,
+                                    const int64_t* __restrict__ rs, int32_t* __restrict__ cur,
+                                    int32_t* __restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = (int32_t)edges[2 * i], c = (int32_t)edges[2 * i + 1];
+    if (a == c) continue;
+    buf[rs[a] + atomicAdd(&cur[a], 1)] = c;
+    buf[rs[c] + atomicAdd(&cur[c], 1)] = a;
+  }
+}
+
+// Sort 32*E entries of one row in registers, keep the first of each run of
+// equal values, write them compacted to the row's start; returns the count.
+template <int E>
+__device__ __forceinline__ int canon_row(int32_t* __restrict__ buf, int64_t b, int d, int lane) {
+  int32_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int idx = lane * E + e;
+    x[e] = idx < d ? buf[b + idx] : 0x7fffffff;
+  }
+  warp_bitonic<E>(x, lane);
+  const int32_t prev_last = __shfl_up_sync(0xffffffffu, x[E - 1], 1);
+  unsigned keep = 0;
+  int c = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int idx = lane * E + e;
+    const int32_t p = e ? x[e - 1] : (lane ? prev_last : (int32_t)0x80000000);
+    const bool k = idx < d && x[e] != p;
+    keep |= (unsigned)k << e;
+    c += k;
+  }
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int pos = incl - c;
+  __syncwarp();  // every lane has read the row before any writes it back
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if ((keep >> e) & 1u) buf[b + pos++] = x[e];
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// one warp per row; rows longer than REORDER_REG listed for k_canon_long_rows
+__global__ void __launch_bounds__(256)
+k_canon_rows(const int64_t* __restrict__ rs, int64_t n, int32_t* __restrict__ buf,
+             int32_t* __restrict__ ucnt, int64_t* __restrict__ seg_v,
+             unsigned long long* __restrict__ nlong) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t b = rs[v];
+    const int d = (int)(rs[v + 1] - b);
+    int u;
+    if (d == 0) u = 0;
+    else if (d <= 32) u = canon_row<1>(buf, b, d, lane);
+    else if (d <= 64) u = canon_row<2>(buf, b, d, lane);
+    else if (d <= 128) u = canon_row<4>(buf, b, d, lane);
+    else if (d <= REORDER_REG) u = canon_row<8>(buf, b, d, lane);
+    else {
+      if (lane == 0) seg_v[atomicAdd(nlong, 1ull)] = v;
+      continue;
+    }
+    if (lane == 0) ucnt[v] = u;
+  }
+}
+
+// the long rows: one CTA each, bitonic sort in shared memory, deduplicated
+__global__ void __launch_bounds__(LONGROW_THREADS)
+k_canon_long_rows(const int64_t* __restrict__ rs, int32_t* __restrict__ buf,
+                  int32_t* __restrict__ ucnt, const int64_t* __restrict__ seg_v,
+                  const unsigned long long* __restrict__ nlong) {
+  extern __shared__ int32_t sb[];
+  __shared__ int wsum[LONGROW_THREADS / 32];
+  const unsigned long long cnt = *nlong;
+  for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
+    const int64_t v = seg_v[r];
+    const int64_t b = rs[v];
+    const int len = (int)(rs[v + 1] - b);
+    int p2 = 256;
+    while (p2 < len) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) sb[i] = i < len ? buf[b + i] : 0x7fffffff;
+    __syncthreads();
+    for (int k = 2; k <= p2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+          const int ij = i ^ j;
+          if (ij > i) {
+            const int32_t x = sb[i], y = sb[ij];
+            if ((x > y) == ((i & k) == 0)) {
+              sb[i] = y;
+              sb[ij] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // compact the first of each run: block-wide prefix over chunks of blockDim
+    int base = 0;
+    for (int i0 = 0; i0 < len; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const bool k = i < len && (i == 0 || sb[i] != sb[i - 1]);
+      const int32_t val = k ? sb[i] : 0;
+      const unsigned bm = __ballot_sync(0xffffffffu, k);
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      if (lane == 0) wsum[w] = __popc(bm);
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+        if (q < w) before += wsum[q];
+        tot += wsum[q];
+      }
+      if (k) buf[b + base + before + __popc(bm & ((1u << lane) - 1))] = val;
+      base += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) ucnt[v] = base;
+    __syncthreads();
+  }
+}
+
+// row v's ucnt[v] deduplicated entries from buf[rs[v] ..) to col[ro[v] ..)
+__global__ void k_compact_rows(const int64_t* __restrict__ rs, const int64_t* __restrict__ ro,
+                               const int32_t* __restrict__ buf, int64_t n,
+                               int32_t* __restrict__ col) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t src = rs[v], dst = ro[v];
+    const int d = (int)(ro[v + 1] - dst);
+    for (int i = lane; i < d; i += 32) col[dst + i] = buf[src + i];
+  }
+}
+
+__global__ void k_widen32(const int32_t* __restrict__ src, int64_t count, int64_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void k_max_i32(const int32_t* __restrict__ x, int64_t count, int* __restrict__ out) {
+  int mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, x[i]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
+// Row-wise canonical CSR of g from device edges (two host waits: the
+// counts' maximum, then the deduplicated total).  Returns 1 -- nothing
+// changed -- when a vertex has more than CANON_ROWS_MAX_DEG endpoints: the
+// key sort handles hubs better (ba200k's 7.6 k-entry rows: 0.57 ms by key
+// sort, 0.70 ms by rows; planted1m, all rows <= 256: 3.09 -> 2.78 ms and
+// steadier).  -2 for an id outside [0, n).
+constexpr int CANON_ROWS_MAX_DEG = 2048;
+static_assert(CANON_ROWS_MAX_DEG <= LONGROW_MAX, "long canonical rows are sorted by one CTA");
+template <typename T>
+int canon_rows(mce_graph* g, const T* d_edges, int64_t num_edges, cudaStream_t s) {
+  const int64_t n = g->n;
+  int32_t *cnt = nullptr, *cur = nullptr, *buf = nullptr, *ucnt = nullptr;
+  int64_t *rs = nullptr, *seg = nullptr;
+  int* flags = nullptr;  // [0] out of range, [1] max endpoints per vertex
+  unsigned long long* nlong = nullptr;
+  if (dev_alloc(&cnt, n, s) || dev_alloc(&flags, 2, s)) return -1;
+  MCE_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, s));
+  MCE_CHECK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+  k_count_endpoints<T><<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, n, cnt, flags);
+  mce_count_launch();
+  k_max_i32<<<grid_for(n), 256, 0, s>>>(cnt, n, flags + 1);
+  mce_count_launch();
+  int hf[2] = {0, 0};
+  MCE_CHECK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaStreamSynchronize(s));
+  dev_free(flags, s);
+  if (hf[0]) {
+    dev_free(cnt, s);
+    mce_set_error("vertex id outside [0, num_vertices)");
+    return -2;
+  }
+  if (hf[1] > CANON_ROWS_MAX_DEG) {
+    dev_free(cnt, s);
+    return 1;
+  }
+  // row starts of the raw (duplicate-carrying) rows
+  if (dev_alloc(&rs, n + 1, s)) return -1;
+  MCE_CHECK(cudaMemsetAsync(rs + n, 0, sizeof(int64_t), s));
+  k_widen32<<<grid_for(n), 256, 0, s>>>(cnt, n, rs);
+  mce_count_launch();
+  size_t tb = 0;
+  MCE_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, rs, rs, n + 1, s));
+  void* tmp = nullptr;
+  MCE_CHECK(cudaMallocAsync(&tmp, tb, s));
+  MCE_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, rs, rs, n + 1, s));
+  cur = cnt;  // reused as the scatter cursors
+  MCE_CHECK(cudaMemsetAsync(cur, 0, sizeof(int32_t) * n, s));
+  if (dev_alloc(&buf, 2 * num_edges, s) || dev_alloc(&ucnt, n, s) || dev_alloc(&seg, n + 1, s))
+    return -1;
+  nlong = reinterpret_cast<unsigned long long*>(seg + n);
+  MCE_CHECK(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), s));
+  k_scatter_endpoints<T><<<grid_for(num_edges), 256, 0, s>>>(d_edges, num_edges, rs, cur, buf);
+  mce_count_launch();
+  k_canon_rows<<<grid_for(n * 32), 256, 0, s>>>(rs, n, buf, ucnt, seg, nlong);
+  mce_count_launch();
+  static bool attr = false;
+  if (!attr) {
+    MCE_CHECK(cudaFuncSetAttribute(k_canon_long_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(LONGROW_MAX * sizeof(int32_t))));
+    attr = true;
+  }
+  k_canon_long_rows<<<296, LONGROW_THREADS, LONGROW_MAX * sizeof(int32_t), s>>>(rs, buf, ucnt, seg,
+                                                                                nlong);
+  mce_count_launch();
+  // final row offsets (the deduplicated counts' exclusive sum)
+  if (dev_alloc(&g->ro, n + 1, s)) return -1;
+  MCE_CHECK(cudaMemsetAsync(g->ro + n, 0, sizeof(int64_t), s));
+  k_widen32<<<grid_for(n), 256, 0, s>>>(ucnt, n, g->ro);
+  mce_count_launch();
+  MCE_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, g->ro, g->ro, n + 1, s));
+  int64_t nnz = 0;
+  MCE_CHECK(cudaMemcpyAsync(&nnz, g->ro + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  MCE_CHECK(cudaStreamSynchronize(s));
+  g->nnz = nnz;
+  if (dev_alloc(&g->col, std::max<int64_t>(nnz, 1), s)) return -1;
+  if (nnz > 0) {
+    k_compact_rows<<<grid_for(n * 32), 256, 0, s>>>(rs, g->ro, buf, n, g->col);
+    mce_count_launch();
+  }
+  MCE_CHECK(cudaGetLastError());
+  cudaFreeAsync(tmp, s);
+  dev_free(cnt, s);
+  dev_free(rs, s);
+  dev_free(buf, s);
+  dev_free(ucnt, s);
+  dev_free(seg, s);
+  return mce_graph_build_split(g, s);
+}
+
 int csr_from_sorted_keys(mce_graph* g, uint64_t* keys, int64_t nnz, int b, cudaStream_t s) {
   g->nnz = nnz;
   if (dev_alloc(&g->ro, g->n + 1, s)) return -1;
@@ -1758,6 +1998,16 @@ int from_edges_impl(const T* edges, int64_t num_edges, int64_t num_vertices, int
     MCE_CHECK(cudaMemcpyAsync(owned, edges, sizeof(T) * 2 * num_edges,
                               cudaMemcpyHostToDevice, s));
     d_edges = owned;
+  }
+  const char* ks = getenv("MCE_CANON_KEYSORT");  // diagnostics: 1 = always the key sort
+  if (num_edges > 0 && !(ks && atoi(ks) != 0)) {
+    const int rc = canon_rows(g, d_edges, num_edges, s);
+    if (rc != 1) {  // done (0) or an error; 1 = a row too long for the row path
+      dev_free(owned, s);
+      if (rc) delete g;
+      else *out = g;
+      return rc;
+    }
   }
   uint64_t* keys = nullptr;
   int64_t m = 0;

@@ -377,3 +377,32 @@ def test_criterion_4_graph_set(i, monkeypatch):
                     donated += res.donation_count
     # (these sparse graphs' subtrees are too small to donate: phase 2 finds no
     # branch with |P| >= donation_min_p -- as in the reference's own run)
+
+
+@pytest.mark.parametrize("variant", ["rows", "keysort"])
+def test_from_edges_canonical_csr_with_duplicates_loops_and_hubs(variant, monkeypatch):
+    """from_edges (graph.py:103-129): duplicates in either orientation and
+    self-loops dropped, rows strictly ascending -- on both canonicalisation
+    paths (row-wise; the key sort, which also takes every graph with a vertex
+    of more than 2048 endpoints), rows of every register class, a long row
+    sorted by one CTA, and a hub past the row path's limit."""
+    if variant == "keysort":
+        monkeypatch.setenv("MCE_CANON_KEYSORT", "1")
+    rng = np.random.default_rng(11)
+    n = 30_000
+    parts = [rng.integers(0, n, size=(60_000, 2))]                  # random, some loops
+    parts.append(parts[0][:5000][:, ::-1])                          # reversed duplicates
+    parts.append(parts[0][:3000])                                   # exact duplicates
+    parts.append(np.column_stack((np.full(1500, 7), rng.integers(0, n, 1500))))   # row > 256
+    parts.append(np.column_stack((np.full(400, 9), np.full(400, 9))))             # loops only
+    hub = np.column_stack((np.full(20_000, 5), np.arange(10, 20_010) % n))  # > the row path's 2048
+    for with_hub in (False, True):
+        edges = np.concatenate(parts + ([hub, hub[:100]] if with_hub else [])).astype(np.int64)
+        g = from_edges(edges, n)
+        ro, ci = oracle.from_edges(edges, n)
+        assert np.array_equal(g.row_offsets, ro)
+        assert np.array_equal(g.col_indices, ci)
+        g32 = from_edges(edges.astype(np.int32), n)
+        assert np.array_equal(g32.col_indices, ci)
+    with pytest.raises(ValueError):
+        from_edges(np.array([[0, n]], dtype=np.int64), n)

@@ -27,6 +27,9 @@
 // carry a big search tree).
 
 constexpr int TINY_WARPS = 8;
+#ifndef MCE_TINY_U
+#define MCE_TINY_U 4  // entry loads per lane in flight in the build walk
+#endif
 constexpr int64_t TINY_MIN_ROOTS = 8192;  // smaller W = 1 classes stay on the warp kernel
 constexpr int TINY_THREADS = 32 * TINY_WARPS;
 #ifndef MCE_TINY_XT
@@ -385,7 +388,7 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
       }
       const int exc2 = inc2 - len;
       const int tot2 = __shfl_sync(FULLMASK, inc2, 31);
-      constexpr int U = 4;
+      constexpr int U = MCE_TINY_U;
       for (int b2 = 0; b2 < tot2; b2 += 32 * U) {
         int32_t val[U];
         int inf[U];

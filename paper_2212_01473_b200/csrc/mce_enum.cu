@@ -53,6 +53,10 @@ namespace {
 #define MCE_CMP_NARROW_MAX_W 1
 #endif
 constexpr int HIST_SMEM = 128;
+#ifndef MCE_TEAM_REMOTE_MIN_P
+#define MCE_TEAM_REMOTE_MIN_P 48
+#endif
+constexpr int TEAM_REMOTE_MIN_P = MCE_TEAM_REMOTE_MIN_P;
 constexpr int CMP_WORDS = 256;  // per-warp compact_run scratch: 64 + 64 ints, 64 x 8-byte rows
 constexpr int HIST_MAX = MCE_HIST_MAX;
 constexpr unsigned FULLMASK = 0xffffffffu;
@@ -93,7 +97,8 @@ struct Mailbox {
   int32_t owner;    // worker whose buffers hold the root's induced rows
   int32_t np, nx;   // the root's |P| and |X|
   int32_t xr;       // X rows in use for the root
-  int32_t pad;
+  int32_t pubcta;   // team classes: -1 = a CTA-mate's branch (rows shared), else the donor
+                    // CTA whose published rows the receiving team copies (a takeover)
 };  // the branch's P and X_P bitsets go to EnumArgs::mbits (2W words per worker)
 
 struct EnumArgs {
@@ -135,8 +140,9 @@ struct EnumArgs {
   int* wl_wake;
   Mailbox* mbox;
   uint32_t* mbits;
-  uint32_t* pub;  // shared-memory-row classes: per worker, the root's rows + plist published
-                  // for the receivers of its branches (W * CAPP + CAP words)
+  uint32_t* pub;  // shared-memory-row classes: per worker (per CTA for teams), the root's rows +
+                  // plist published for the receivers of its branches (W * CAPP + CAP words)
+  unsigned* pub_refs;  // teams: per CTA, takeovers still copying its published rows
   int worker_list_on;
   int min_p;
   int min_x;  // also donate branches whose node has >= min_x live X_X members (0: off)
@@ -230,7 +236,15 @@ struct Bits {
   uint32_t w[K];
 };
 
-template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM>
+// TEAM = T > 0: the paper's thread-block worker.  The T warps of a CTA
+// share ONE copy of the root's induced rows in shared memory; warp 0 claims
+// and builds the roots, and a busy warp hands branches to idle CTA-mates at
+// any time (no row copy: the rows are the CTA's).  Across CTAs, in phase 2
+// a branch goes only to a team whose T warps are all idle (a takeover): its
+// warp 0 copies the branch's candidate rows from the donor team's published
+// copy into the team's shared memory, then shares the branch out the same
+// way.  T divides 32, so a team's idle bits sit in one word of idle_bits.
+template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int TEAM = 0>
 struct Worker {
   static constexpr int CAP = 32 * W;
   static constexpr int CAPP = CAP + 1;
@@ -279,6 +293,12 @@ struct Worker {
   unsigned long long cliques = 0, hash = 0, max_size = 0;
   bool phase2_seen = false;
   int64_t nroots = 0;  // a.num_roots, or the count an earlier kernel left in a.num_roots_dev
+  // teams
+  int cta = 0, tw = 0;          // team (CTA) index, warp within the team
+  int team_word = 0, team_shift = 0;
+  int* s_pub = nullptr;         // shared: 0 rows not published, 1 publishing, 2 published
+  bool counted = true;          // this park counts toward termination (false: a leader
+                                // waiting for its team in phase 1)
 
   __device__ Worker(const EnumArgs& args, int lane_, int wid_, uint32_t* smem_rows,
                     int32_t* smem_plist, uint32_t* smem_p, unsigned int* smem_hist,
@@ -294,6 +314,13 @@ struct Worker {
       plist = a.plist_g + (size_t)wid * CAP;
     }
     nroots = a.num_roots_dev ? (int64_t)*(volatile const unsigned long long*)a.num_roots_dev : a.num_roots;
+    if (TEAM) {
+      constexpr int TT = TEAM > 0 ? TEAM : 1;
+      cta = wid / TT;
+      tw = wid % TT;
+      team_word = (cta * TT) >> 5;
+      team_shift = (cta * TT) & 31;
+    }
     xrows_own = XROWS ? a.xrows + (size_t)wid * W * a.xcap : nullptr;
     xrowsT = xrows_own;
     xstride = a.xcap;
@@ -882,7 +909,11 @@ struct Worker {
   // donate the branch (v, childP, childXP) to an idle worker (scheduler.py:417-438)
   __device__ bool try_donate(const B& childP, const B& childXP, int v, int32_t gv, int live,
                              int rlen) {
-    const int rid = claim_receiver();
+    bool takeover = false;
+    // a takeover copies the branch's candidate rows into the taking team:
+    // only branches big enough to pay for it leave the team
+    const int rid = TEAM ? claim_team_receiver(takeover, popc(childP) >= TEAM_REMOTE_MIN_P)
+                         : claim_receiver();
     if (rid < 0) return false;
     // receiver's X_X: the live tokens adjacent to v, in prefix order
     int32_t* rx = a.xx + (size_t)rid * a.xcap;
@@ -895,8 +926,69 @@ struct Worker {
       if (keep) rx[k + __popc(km & lt)] = xx[i];
       k += __popc(km);
     }
-    send_branch(rid, childP, childXP, gv, rlen, k);
+    send_branch(rid, childP, childXP, gv, rlen, k, takeover);
     return true;
+  }
+
+  // teams: an idle CTA-mate (local), else -- in phase 2 -- the warp 0 of a
+  // fully idle team, all T of its bits taken at once (a takeover)
+  __device__ int claim_team_receiver(bool& takeover, bool remote_ok) {
+    takeover = false;
+    constexpr unsigned TM = TEAM >= 32 ? ~0u : ((1u << (TEAM > 0 ? TEAM : 1)) - 1u);
+    int rid = -1;
+    if (lane == 0) {
+      const unsigned mates = (TM << team_shift) & ~(1u << (team_shift + tw));
+      unsigned bits = *(volatile unsigned*)&a.idle_bits[team_word] & mates;
+      while (bits && rid < 0) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const unsigned old = atomicAnd(&a.idle_bits[team_word], ~(1u << b));
+        if (old & (1u << b)) {
+          rid = team_word * 32 + b;
+          atomicAdd(&a.wl->state, 1ull);  // one more donation in flight
+        }
+      }
+    }
+    rid = __shfl_sync(FULLMASK, rid, 0);
+    if (rid >= 0 || !remote_ok || !phase2()) return rid;
+    const unsigned long long st = *(volatile unsigned long long*)&a.wl->state;
+    if ((st >> 32) + 1 < (unsigned long long)TEAM + 1) return -1;  // no whole team can be idle
+    const int nwords = (a.num_workers + 31) >> 5;
+    const int start = (cta * 7) % nwords;
+    for (int base = 0; base < nwords && rid < 0; base += 32) {
+      const int wi = (start + base + lane) % nwords;
+      const unsigned bits = (base + lane < nwords) ? *(volatile unsigned*)&a.idle_bits[wi] : 0u;
+      unsigned full = 0;  // fully idle teams in this word (not mine)
+#pragma unroll
+      for (int sh = 0; sh < 32; sh += (TEAM > 0 ? TEAM : 32))
+        if (((bits >> sh) & TM) == TM && !(wi == team_word && sh == team_shift)) full |= 1u << sh;
+      unsigned m = __ballot_sync(FULLMASK, full != 0);
+      while (m && rid < 0) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const unsigned f = __shfl_sync(FULLMASK, full, src);
+        const int wordi = __shfl_sync(FULLMASK, wi, src);
+        int claimed = -1;
+        if (lane == 0) {
+          for (unsigned t = f; t && claimed < 0; t &= t - 1) {
+            const int sh = __ffs(t) - 1;
+            unsigned cur = *(volatile unsigned*)&a.idle_bits[wordi];
+            while (((cur >> sh) & TM) == TM) {
+              const unsigned seen = atomicCAS(&a.idle_bits[wordi], cur, cur & ~(TM << sh));
+              if (seen == cur) {
+                claimed = wordi * 32 + sh;
+                atomicAdd(&a.wl->state, 1ull);
+                break;
+              }
+              cur = seen;
+            }
+          }
+        }
+        rid = __shfl_sync(FULLMASK, claimed, 0);
+      }
+    }
+    takeover = rid >= 0;
+    return rid;
   }
 
   // claim an idle worker off the worker list (-1: none parked)
@@ -933,7 +1025,7 @@ struct Worker {
   // hand the claimed worker `rid` the branch (its X_X tokens, nxx of them,
   // are already in its xx buffer): R path, P / X_P bitsets, the root's rows
   __device__ void send_branch(int rid, const B& childP, const B& childXP, int32_t gv, int rlen,
-                              int nxx) {
+                              int nxx, bool takeover = false) {
     Mailbox* mb = a.mbox + rid;
     uint32_t* mbits = a.mbits + (size_t)rid * 2 * W;
     int32_t* rr = a.rpath + (size_t)rid * (a.levels + 2);
@@ -945,7 +1037,30 @@ struct Worker {
         mbits[W + word(q)] = childXP.w[q];
       }
     }
-    if (ROWS_SMEM && !published) {  // first donation from this root: publish its rows
+    if (TEAM) {
+      if (takeover) {  // the team's rows, published once per context, for the taking team
+        int st = 0;
+        if (lane == 0) st = atomicCAS(s_pub, 0, 1);
+        st = __shfl_sync(FULLMASK, st, 0);
+        if (st == 0) {
+          if (lane == 0)  // the previous context's takeovers have copied their rows
+            while (*(volatile unsigned*)&a.pub_refs[cta]) __nanosleep(64);
+          __syncwarp();
+          uint32_t* pb = a.pub + (size_t)cta * (W * CAPP + CAP);
+          for (int w = 0; w < W; ++w)
+            for (int c = lane; c < np; c += 32) pb[w * CAPP + c] = rowsT[w * CAPP + c];
+          for (int c = lane; c < np; c += 32) pb[W * CAPP + c] = plist[c];
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicExch(s_pub, 2);
+        } else {
+          if (lane == 0)
+            while (*(volatile int*)s_pub != 2) __nanosleep(32);
+          __syncwarp();
+        }
+        if (lane == 0) atomicAdd(&a.pub_refs[cta], 1u);
+      }
+    } else if (ROWS_SMEM && !published) {  // first donation from this root: publish its rows
       uint32_t* pb = a.pub + (size_t)wid * (W * CAPP + CAP);
       for (int w = 0; w < W; ++w)
         for (int c = lane; c < np; c += 32) pb[w * CAPP + c] = rowsT[w * CAPP + c];
@@ -961,6 +1076,7 @@ struct Worker {
       mb->np = np;
       mb->nx = nx;
       mb->xr = xr ? 1 : 0;
+      mb->pubcta = TEAM && takeover ? cta : -1;
       mb->has_task = 1;
     }
     __threadfence();
@@ -1001,6 +1117,58 @@ struct Worker {
     got = __shfl_sync(FULLMASK, got, 0);
     __threadfence();
     return got != 0;
+  }
+
+  // teams: park until handed a branch (1) or terminated (0); a leader in
+  // phase 1 (`leader_wait`) parks uncounted -- it cannot end the launch --
+  // and returns 2 once every CTA-mate is parked with nothing in flight to it
+  // (it has then left the idle set: the shared rows are its to rebuild)
+  __device__ int park_team(bool leader_wait) {
+    constexpr unsigned TM = TEAM >= 32 ? ~0u : ((1u << (TEAM > 0 ? TEAM : 1)) - 1u);
+    int got = 0;
+    if (lane == 0) {
+      WorkerListDev* wl = a.wl;
+      const unsigned me = 1u << (wid & 31);
+      bool fin = false;
+      if (!leader_wait) {
+        const unsigned long long now = atomicAdd(&wl->state, 1ull << 32) + (1ull << 32);
+        if ((now >> 32) == (unsigned long long)a.num_workers && (now & 0xffffffffull) == 0) {
+          atomicExch(&wl->terminated, 1);  // last one in with nothing in flight
+          fin = true;
+        }
+      }
+      if (!fin) {
+        atomicOr(&a.idle_bits[wid >> 5], me);
+        const unsigned mates = (TM << team_shift) & ~me;
+        unsigned ns = 32;
+        for (;;) {
+          if (*(volatile int*)&a.wl_wake[wid]) {
+            got = 1;
+            break;
+          }
+          if (!leader_wait && *(volatile int*)&wl->terminated) break;
+          if (leader_wait && (*(volatile unsigned*)&a.idle_bits[team_word] & mates) == mates) {
+            const unsigned old = atomicAnd(&a.idle_bits[team_word], ~me);
+            if (old & me) {
+              got = 2;
+              break;
+            }  // else claimed by a donor: its branch is on the way
+          }
+          __nanosleep(ns);
+          ns = ns < 1024 ? ns * 2 : ns;
+        }
+        if (got == 1) {
+          __threadfence();
+          a.wl_wake[wid] = 0;
+          a.mbox[wid].has_task = 0;
+          // retire the in-flight donation (and leave the idle count when counted)
+          atomicAdd(&wl->state, leader_wait ? ~0ull : ~0ull - (1ull << 32));
+        }
+      }
+    }
+    got = __shfl_sync(FULLMASK, got, 0);
+    __threadfence();
+    return got;
   }
 
   // ---------------------------------------------------------------- compact subtrees
@@ -1271,7 +1439,7 @@ struct Worker {
       const int32_t gv = __shfl_sync(FULLMASK, vh2 ? gvs[H - 1] : gvs[0], vl);
       const uint64_t vhv = __shfl_sync(FULLMASK, vh2 ? vh[H - 1] : vh[0], vl);
       if (a.worker_list_on && (popcm(childP) >= a.min_p || (a.min_x > 0 && live >= a.min_x)) &&
-          below > 0 && NL != 0 && phase2()) {
+          below > 0 && NL != 0 && (TEAM > 0 || phase2())) {
         if (donate_compact<M, H>(childP, XP & rowv, v, gv, live, rlen, cid, nu, xrow, tok)) continue;
       }
       // stable partition of the live X_X prefix by adjacency to v (xsets.py:55-82)
@@ -1383,7 +1551,9 @@ struct Worker {
       cXP.w[k] = valid(k, lane) ? sXP[word(k)] : 0u;
     }
     __syncwarp();
-    const int rid = claim_receiver();
+    bool takeover = false;
+    const int rid = TEAM ? claim_team_receiver(takeover, popcm(childP) >= TEAM_REMOTE_MIN_P)
+                         : claim_receiver();
     if (rid < 0) return false;
     int32_t* rx = a.xx + (size_t)rid * a.xcap;
     const unsigned lt = (1u << lane) - 1;
@@ -1396,7 +1566,7 @@ struct Worker {
       if (keep) rx[k + __popc(km & lt)] = tok[h];
       k += __popc(km);
     }
-    send_branch(rid, cP, cXP, gv, rlen, k);
+    send_branch(rid, cP, cXP, gv, rlen, k, takeover);
     return true;
   }
 
@@ -1504,7 +1674,7 @@ struct Worker {
       const int cpop = popc(childP);
       const int32_t gv = plist[v];
       if (a.worker_list_on && (cpop >= a.min_p || (a.min_x > 0 && live >= a.min_x)) &&
-          below > 0 && any(NL) && phase2()) {
+          below > 0 && any(NL) && (TEAM > 0 || phase2())) {
         B cxp;
 #pragma unroll
         for (int k = 0; k < K; ++k) cxp.w[k] = XP.w[k] & rowv.w[k];
@@ -1626,10 +1796,13 @@ struct Worker {
     const int64_t r = a.roots_mode == 1 ? (r_enc & ROOT_ID_MASK) : r_enc;
     const int heavy = a.roots_mode == 1 ? (int)(r_enc >> ROOT_ID_BITS) : 0;
     root_x = a.roots_mode == 1 ? a.col + a.ro[r] : a.xlist + (size_t)owner * a.xcap;
-    if (ROWS_SMEM) {
+    if (TEAM && mb->pubcta < 0) {
+      // a CTA-mate's branch: the rows are this team's shared rows already
+    } else if (ROWS_SMEM) {
       // only the rows of the branch's candidates (P | X_P) are ever read below
       // this node: copy those (lane per candidate), and the member list
-      const uint32_t* pb = a.pub + (size_t)owner * (W * CAPP + CAP);
+      const int src = TEAM ? mb->pubcta : owner;
+      const uint32_t* pb = a.pub + (size_t)src * (W * CAPP + CAP);
       const uint32_t* mbits = a.mbits + (size_t)wid * 2 * W;
       for (int k = 0; k < W; ++k) {
         const uint32_t cw = mbits[k] | mbits[W + k];  // broadcast read
@@ -1639,6 +1812,17 @@ struct Worker {
         }
       }
       for (int c = lane; c < np; c += 32) plist[c] = (int32_t)pb[W * CAPP + c];
+      if (TEAM) {  // a takeover: this team's shared rows now hold the branch
+        constexpr unsigned TM = TEAM >= 32 ? ~0u : ((1u << (TEAM > 0 ? TEAM : 1)) - 1u);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          atomicSub(&a.pub_refs[src], 1u);
+          *s_pub = 0;  // a new context: its rows are not published yet
+          // the CTA-mates (parked, their bits taken by the takeover) receive again
+          atomicOr(&a.idle_bits[team_word], (TM << team_shift) & ~(1u << (wid & 31)));
+        }
+      }
     } else {
       rowsT = a.rows_g + (size_t)owner * W * CAPP;
       plist = a.plist_g + (size_t)owner * CAP;
@@ -1699,8 +1883,17 @@ struct MinBlocks {
                                : W == 32 ? MCE_MINB_W32 : 1;
 };
 
-template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(EnumArgs a) {
+// teams (T > 0) hold one shared copy of the rows per CTA; their residency is
+// bounded by shared memory (W = 32: 135 KB) or registers
+template <int W, int TEAM>
+struct MinBlocksT {
+  static constexpr int value = TEAM == 0 ? MinBlocks<W>::value : (W >= 32 ? 1 : 3);
+};
+
+template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS, int TEAM = 0>
+__global__ void __launch_bounds__(WARPS * 32, MinBlocksT<W, TEAM>::value) k_enumerate(EnumArgs a) {
+  static_assert(TEAM == 0 || (TEAM == WARPS && 32 % (TEAM > 0 ? TEAM : 1) == 0 && ROWS_SMEM),
+                "team = one CTA");
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
   constexpr int SPW = W < 32 ? 32 : W;  // sP words per warp
@@ -1709,18 +1902,23 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
   uint32_t* s_p = reinterpret_cast<uint32_t*>(s_hist + HIST_SMEM);
   int32_t* s_cmp = reinterpret_cast<int32_t*>(s_p + 3 * WARPS * SPW);  // CMP_WORDS per warp
   uint32_t* s_rows = reinterpret_cast<uint32_t*>(s_cmp + WARPS * CMP_WORDS);
-  int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? WARPS * W * CAPP : 0));
+  constexpr int RCOPIES = TEAM ? 1 : WARPS;  // row copies in shared memory
+  int32_t* s_plist = reinterpret_cast<int32_t*>(s_rows + (ROWS_SMEM ? RCOPIES * W * CAPP : 0));
+  __shared__ int s_pubstate;  // teams: the shared rows' publication state
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x) s_hist[i] = 0;
+  if (threadIdx.x == 0) s_pubstate = 0;
   __syncthreads();
   const int wid = blockIdx.x * WARPS + warp;
   if (wid < a.num_workers) {
-    Worker<W, PIVOT_XX, XROWS, ROWS_SMEM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? warp * W * CAPP : 0),
-                                  s_plist + (ROWS_SMEM ? warp * CAP : 0), s_p + 3 * warp * SPW,
+    const int rc = TEAM ? 0 : warp;
+    Worker<W, PIVOT_XX, XROWS, ROWS_SMEM, TEAM> wk(a, lane, wid, s_rows + (ROWS_SMEM ? rc * W * CAPP : 0),
+                                  s_plist + (ROWS_SMEM ? rc * CAP : 0), s_p + 3 * warp * SPW,
                                   s_hist, s_cmp + warp * CMP_WORDS);
+    wk.s_pub = &s_pubstate;
     int stripe = wid % ROOT_STRIPES;
-    bool phase1 = true;
+    bool phase1 = TEAM ? warp == 0 : true;  // a team's warp 0 claims and builds its roots
     const long long t_start = clock64();
     // launch phase times with few same-address atomics: the start by one thread,
     // the first root-list miss and the last end only while they can still move
@@ -1732,7 +1930,39 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
       Bits<W> P, XP;
       int nxx = 0, rlen = 0;
       int64_t idx = -1;
-      if (phase1) {
+      bool from_root = false;
+      if (TEAM) {
+        long long t0 = wk.tic();
+        // phase 1 (warp 0): wait for the team to go idle -- taking CTA-mates'
+        // branches meanwhile -- then claim and build the next root
+        const int r = wk.park_team(phase1);
+        wk.toc(T_WLIST, t0);
+        if (r == 0) break;
+        if (r == 2) {
+          t0 = wk.tic();
+          idx = wk.claim_root(stripe);
+          wk.toc(T_WLIST, t0);
+          if (idx < 0) {
+            phase1 = false;
+            if (a.phase_ns && lane == 0 && !*(volatile unsigned long long*)&a.phase_ns[1])
+              atomicMax(&a.phase_ns[1], ~gtimer());
+            continue;
+          }
+          wk.roots_claimed++;
+          if (lane == 0) s_pubstate = 0;  // a new context in the shared rows
+          __syncwarp();
+          t0 = wk.tic();
+          rlen = wk.prepare_root(a.roots[idx], P, XP, nxx);
+          wk.toc(T_BUILD, t0);
+          from_root = true;
+        } else {
+          wk.don_recv++;
+          t0 = wk.tic();
+          rlen = wk.prepare_donated(P, XP, nxx);
+          wk.toc(T_BUILD, t0);
+        }
+      } else if (phase1) {
+        from_root = true;
         long long t0 = wk.tic();
         idx = wk.claim_root(stripe);
         wk.toc(T_WLIST, t0);
@@ -1758,8 +1988,8 @@ __global__ void __launch_bounds__(WARPS * 32, MinBlocks<W>::value) k_enumerate(E
         wk.toc(T_BUILD, t0);
       }
       const long long t0 = a.root_cycles ? clock64() : 0;
-      wk.traverse(P, XP, nxx, rlen, phase1);
-      if (phase1 && a.root_cycles && lane == 0) a.root_cycles[idx] = clock64() - t0;
+      wk.traverse(P, XP, nxx, rlen, from_root);
+      if (from_root && a.root_cycles && lane == 0) a.root_cycles[idx] = clock64() - t0;
     }
     if (lane == 0) {
       atomicAdd(&a.g_acc[0], wk.cliques);
@@ -2061,17 +2291,18 @@ struct ClassPlan {
   int64_t begin, count;  // slice of the sorted root list
 };
 
-template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS>
+template <int W, bool PIVOT_XX, bool XROWS, bool ROWS_SMEM, int WARPS, int TEAM = 0>
 int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cudaStream_t s,
                  int64_t* launches, size_t mem_budget, cudaEvent_t* ev, bool* xrows_used,
                  Scratch& scr) {
   constexpr int CAP = 32 * W;
   constexpr int CAPP = CAP + 1;
-  auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS>;
+  auto kern = k_enumerate<W, PIVOT_XX, XROWS, ROWS_SMEM, WARPS, TEAM>;
   constexpr int SPW = W < 32 ? 32 : W;
+  constexpr int RCOPIES = TEAM ? 1 : WARPS;
   size_t smem = HIST_SMEM * sizeof(unsigned int) + 3 * WARPS * SPW * sizeof(uint32_t) +
                 (size_t)WARPS * CMP_WORDS * sizeof(int32_t) +
-                (ROWS_SMEM ? (size_t)WARPS * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
+                (ROWS_SMEM ? (size_t)RCOPIES * (W * CAPP + CAP) * sizeof(uint32_t) : 0);
   if (g_tr) g_tr->mark("class start");
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -2117,6 +2348,10 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   if (requested_workers <= 0 && W < 8)
     workers = std::min<int64_t>(workers, std::max<int64_t>(args.num_roots, 1) + resident / 4);
   workers = std::max<int64_t>(workers, 1);
+  constexpr int TT = TEAM > 0 ? TEAM : 1;
+  if (TEAM)  // whole teams: a requested count rounds up, a resident one down
+    workers = requested_workers > 0 ? std::min<int64_t>((workers + TT - 1) / TT * TT, resident)
+                                    : std::max<int64_t>(TT, workers / TT * TT);
   args.num_workers = (int)workers;
   args.levels = (int)levels;
   args.xcap = xcap;
@@ -2133,7 +2368,8 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   const size_t z_wl = 128;
   const size_t z_wake = (sizeof(int) * (size_t)workers + 127) / 128 * 128;
   const size_t z_idle = (sizeof(unsigned) * (size_t)((workers + 31) / 32) + 127) / 128 * 128;
-  const size_t z_total = z_mbox + z_root + z_wl + z_wake + z_idle;
+  const size_t z_refs = TEAM ? (sizeof(unsigned) * (size_t)(workers / TT) + 127) / 128 * 128 : 0;
+  const size_t z_total = z_mbox + z_root + z_wl + z_wake + z_idle + z_refs;
   unsigned char* zblk = nullptr;
   if (get(&zblk, z_total)) return -1;
   args.root_counter = reinterpret_cast<unsigned long long*>(zblk);
@@ -2141,6 +2377,8 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   args.wl_wake = reinterpret_cast<int*>(zblk + z_root + z_wl);
   args.idle_bits = reinterpret_cast<unsigned*>(zblk + z_root + z_wl + z_wake);
   args.mbox = reinterpret_cast<Mailbox*>(zblk + z_root + z_wl + z_wake + z_idle);
+  args.pub_refs = TEAM ? reinterpret_cast<unsigned*>(zblk + z_root + z_wl + z_wake + z_idle + z_mbox)
+                       : nullptr;
   args.xrows = nullptr;
   args.xlist = nullptr;
   args.rows_g = nullptr;
@@ -2148,7 +2386,8 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   if (XROWS && get(&args.xrows, (size_t)workers * W * xcap)) return -1;
   if (args.roots_mode == 2 && get(&args.xlist, (size_t)workers * xcap)) return -1;
   args.pub = nullptr;
-  if (ROWS_SMEM && args.worker_list_on && get(&args.pub, (size_t)workers * (W * CAPP + CAP)))
+  if (ROWS_SMEM && args.worker_list_on &&
+      get(&args.pub, (size_t)(TEAM ? workers / TT : workers) * (W * CAPP + CAP)))
     return -1;
   if (!ROWS_SMEM && (get(&args.rows_g, (size_t)workers * W * CAPP) ||
                      get(&args.plist_g, (size_t)workers * CAP)))
@@ -2167,6 +2406,17 @@ int launch_class(EnumArgs args, int requested_workers, int64_t* workers_used, cu
   return 0;
 }
 
+// W = 16 / 32 as teams (one shared copy of the rows per CTA; MCE_TEAM=1).
+// Built, parity-tested and measured slower than the per-warp workers, so
+// off by default: on rmat20's core a W = 32 root took 31.6 s as 1 team of 8
+// warps per SM (a takeover copies up to 77 KB of rows; remote branches only
+// from |P| >= 48) against 14.9 s for 12 per-warp workers per SM reading
+// L1/L2-resident rows; W = 8 / 16 chunk 987 vs 981 ms.
+inline bool team(const EnumArgs& a) {
+  const char* e = getenv("MCE_TEAM");
+  return a.worker_list_on && e && atoi(e) != 0;
+}
+
 template <bool PIVOT_XX, bool XROWS>
 int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, int64_t* launches,
              size_t budget, cudaEvent_t* ev, bool* xr, Scratch& scr) {
@@ -2175,8 +2425,12 @@ int launch_W(int W, EnumArgs args, int workers, int64_t* used, cudaStream_t s, i
     case 2: return launch_class<2, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr, scr);
     case 4: return launch_class<4, PIVOT_XX, XROWS, true, 8>(args, workers, used, s, launches, budget, ev, xr, scr);
     case 8: return launch_class<8, PIVOT_XX, XROWS, true, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
-    case 16: return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget, ev, xr, scr);
-    case 32: return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 16:
+      if (team(args)) return launch_class<16, PIVOT_XX, XROWS, true, 4, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
+      return launch_class<16, PIVOT_XX, XROWS, true, 2>(args, workers, used, s, launches, budget, ev, xr, scr);
+    case 32:
+      if (team(args)) return launch_class<32, PIVOT_XX, XROWS, true, 8, 8>(args, workers, used, s, launches, budget, ev, xr, scr);
+      return launch_class<32, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
     case 64: return launch_class<64, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
     case 128: return launch_class<128, PIVOT_XX, XROWS, false, 4>(args, workers, used, s, launches, budget, ev, xr, scr);
   }

@@ -320,3 +320,37 @@ def test_rmat24_sampled_parity():
     core = dict(root_begin=n - 100_000, root_end=n - 100_000 + 64 * 16, root_stride=16)
     res = _check_against_oracle(g2, st, induced="ipx", **core)
     assert res.clique_count > 1_000_000
+
+
+def test_team_workers_match_oracle(monkeypatch):
+    """The thread-block ("team") workers for the W = 16 / 32 classes (opt-in,
+    MCE_TEAM=1): CTA-mates share one copy of the rows, whole idle teams take
+    over branches in phase 2 -- same count, hash and histogram, and with the
+    worker list off the oracle's node total."""
+    monkeypatch.setenv("MCE_TEAM", "1")
+    sizes = [270, 530, 600, 40]
+    parts, base = [], 0
+    for s in sizes:
+        u, v = np.triu_indices(s, k=1)
+        parts.append(np.column_stack((u + base, v + base)))
+        base += s
+    parts.append(k_minus_matching(700, 4) + base)
+    base += 700
+    g = from_edges(np.concatenate(parts).astype(np.int64), base)
+    g2, _, st = preprocess(g)
+    for induced in ("ipx", "ip"):
+        res = run(g2, st, RunConfig(induced=induced, donation_min_p=2))
+        orc = oracle.enumerate_cliques(g2.row_offsets, g2.col_indices, induced=induced,
+                                       degeneracy=st.degeneracy, labels=g2.labels)
+        assert res.clique_count == orc["count"] == len(sizes) + 2 ** 4
+        assert res.clique_hash_hex == orc["hash"] and res.size_histogram == orc["hist"]
+        if induced == "ip":
+            assert res.nodes_total == orc["nodes"]
+    edges, n = generate.workload_edges("rmat20")
+    g2, _, st = preprocess(from_edges(edges, n))
+    sample = dict(root_begin=(1 << 20) - 8576, root_end=(1 << 20) - 7000, root_stride=32)
+    res = run(g2, st, RunConfig(), **sample)
+    orc = oracle.enumerate_cliques(g2.row_offsets, g2.col_indices, induced="ipx",
+                                   degeneracy=st.degeneracy, labels=g2.labels,
+                                   include_isolated=False, **sample)
+    assert (res.clique_count, res.clique_hash_hex) == (orc["count"], orc["hash"])

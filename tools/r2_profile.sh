@@ -12,10 +12,22 @@ timeout -s KILL 600 python bench.py --workload planted1m --impl reference --step
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_planted1m_$tag.csv \
   python bench.py --workload planted1m --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-clocks > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/launches_planted1m_$tag.csv 20 > gpurun_out/launches_planted1m_$tag.txt
+# ncu reports live in /tmp (gpurun copies back at most 64 MiB); their summaries,
+# line tables and the traffic record are made here, on the box
+R=/tmp/ncu_$tag; mkdir -p $R
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k "regex:k_tiny|k_enumerate" -s 3 -c 3 \
-  -o gpurun_out/ncu_enum_planted1m_$tag python tools/diag.py planted1m --reps 2 > /dev/null 2>&1
+  -o $R/ncu_enum_planted1m_$tag python tools/diag.py planted1m --reps 2 > /dev/null 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k "regex:k_tiny|k_enumerate" -s 2 -c 2 \
-  -o gpurun_out/ncu_enum_ba200k_$tag python tools/diag.py ba200k --reps 2 > /dev/null 2>&1
+  -o $R/ncu_enum_ba200k_$tag python tools/diag.py ba200k --reps 2 > /dev/null 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k "regex:k_peel_async" -s 1 -c 1 \
-  -o gpurun_out/ncu_peel_planted1m_$tag python tools/prep_only.py planted1m async 2 > /dev/null 2>&1
-ls gpurun_out | grep $tag
+  -o $R/ncu_peel_planted1m_$tag python tools/prep_only.py planted1m async 2 > /dev/null 2>&1
+for f in ncu_enum_planted1m_$tag ncu_enum_ba200k_$tag ncu_peel_planted1m_$tag; do
+  python tools/ncu_summary.py $R/$f.ncu-rep > gpurun_out/$f.txt 2>&1
+  python tools/ncu_lines.py $R/$f.ncu-rep 40 > gpurun_out/${f}_lines.txt 2>&1
+done
+cp profiles/traffic.json gpurun_out/traffic_$tag.json
+for w in planted1m ba200k; do
+  python tools/traffic_from_ncu.py $w $R/ncu_enum_${w}_$tag.ncu-rep r2/ncu_enum_${w}_$tag.txt > /dev/null 2>&1
+done
+cp profiles/traffic.json gpurun_out/traffic_$tag.json
+ls -la gpurun_out | grep $tag

@@ -271,8 +271,16 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # MCE_BENCH_BACKEND=gloo with more ranks than GPUs: a functional check
+        # of the N > 1 path on one GPU (ranks time-share it) -- never a bench
+        # number; the driver's runs take NCCL and one GPU per rank
+        backend = os.environ.get("MCE_BENCH_BACKEND", "nccl")
+        dev_idx = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
+        torch.cuda.set_device(dev_idx)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2212_01473_b200 import RunConfig, from_device_edges, preprocess
     from paper_2212_01473_b200 import _lib
     from paper_2212_01473_b200.distributed import (run_sharded, run_work_stealing,

@@ -354,3 +354,31 @@ def test_team_workers_match_oracle(monkeypatch):
                                    degeneracy=st.degeneracy, labels=g2.labels,
                                    include_isolated=False, **sample)
     assert (res.clique_count, res.clique_hash_hex) == (orc["count"], orc["hash"])
+
+
+@pytest.mark.parametrize("shard", ["static", "steal"])
+def test_bench_two_ranks_reproduce_one_gpu(shard, tmp_path):
+    """bench.py's N > 1 path end to end: two ranks (torchrun) time-sharing
+    this GPU, gloo standing in for NCCL (MCE_BENCH_BACKEND) -- every rank
+    orders the graph itself, enumerates its shard, and the all-reduced
+    result is the single-GPU clique set exactly."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MCE_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + (shard == "steal")),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "ba200k", "--steps", "3",
+           "--warmup", "3", "--shard", shard, "--no-cpu-baseline", "--no-clocks"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["result"]["sharding"] == shard
+    edges, n = generate.workload_edges("ba200k")
+    g2, _, st = preprocess(from_edges(edges, n))
+    one = run(g2, st, RunConfig())
+    assert line["result"]["maximal_cliques"] == one.clique_count
+    assert line["result"]["clique_hash"] == one.clique_hash_hex

@@ -479,7 +479,170 @@ struct APeelShared {
   int tail_k, tail_degmax, tail_sel;
   unsigned int tail_na;
   alignas(128) unsigned int scans_done;  // k_peel_async1: warps past this level's scan
+  alignas(128) int cert;                  // k_peel_async1: best degeneracy certificate
+  int cert_maxdeg;                        // max degree of the residual it was taken on
+  int cert_k0, cert_k1;                   // diagnostics: threshold before / after the jump
+  unsigned long long cert_t[3];           // diagnostics: globaltimer at start / cert / end
 };
+
+// ---- degeneracy certificate (k_peel_async1's residual jump).  The
+// degeneracy of any subgraph is a lower bound on the graph's degeneracy d,
+// so a level threshold may jump to it: every vertex still leaves with at
+// most threshold <= d later neighbours.  For a sampled live vertex v one CTA
+// computes the degeneracy of G[{v} + live N(v)] (|N(v)| < CERT_M): warp 0
+// lists the members (ascending) and their row offsets in shared memory, all
+// warps build the members' rows as CERT_M-bit bitsets in one flattened walk
+// of their adjacency lists, and warp 0 runs a sequential min-degree peel
+// with warp reductions.  -1 when the neighbourhood is too big.
+constexpr int CERT_M = 128;               // members (v last)
+constexpr int CERT_W = CERT_M / 32;       // bitset words per row
+constexpr int64_t CERT_EMAX = 8192;       // adjacency entries walked per sample
+constexpr int CERT_U = 4;                 // entry loads in flight per thread
+struct CertCta {
+  int32_t mem[CERT_M];      // live neighbours of v, ascending
+  int32_t pre[CERT_M + 1];  // exclusive prefix of the members' row lengths
+  int64_t start[CERT_M];    // row starts
+  unsigned rows[CERT_M * CERT_W];
+  int m, E;                 // members, entries (m < 0: too big)
+};
+
+__device__ __forceinline__ bool cert_live(const unsigned* __restrict__ rbits, int32_t w) {
+  return !((__ldcg(&rbits[w >> 5]) >> (w & 31)) & 1u);
+}
+
+// Called by every thread of the CTA (v uniform); the result is valid in warp 0.
+__device__ int peel_certificate(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                                const unsigned* __restrict__ rbits, int32_t v, CertCta& cw) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  if (threadIdx.x < 32) {
+    // members: the live neighbours (the row is ascending), v gets index m
+    const int64_t r0 = ro[v], r1 = ro[v + 1];
+    int m = r1 - r0 > CERT_EMAX ? -1 : 0;
+    for (int64_t b = r0; m >= 0 && b < r1; b += 32) {
+      const int64_t e = b + lane;
+      const int32_t w = e < r1 ? col[e] : -1;
+      const bool live = w >= 0 && cert_live(rbits, w);
+      const unsigned bl = __ballot_sync(0xffffffffu, live);
+      if (m + __popc(bl) > CERT_M - 1) {
+        m = -1;
+        break;
+      }
+      if (live) cw.mem[m + __popc(bl & lt)] = w;
+      m += __popc(bl);
+    }
+    __syncwarp();
+    // row lengths and starts, exclusive prefix over the members
+    int carry = 0;
+    for (int q = 0; m > 0 && q < CERT_W; ++q) {
+      const int i = lane + 32 * q;
+      int64_t a = 0, len = 0;
+      if (i < m) {
+        a = ro[cw.mem[i]];
+        len = ro[cw.mem[i] + 1] - a;
+        cw.start[i] = a;
+      }
+      const int l32 = (int)(len < CERT_EMAX ? len : CERT_EMAX);
+      int inc = l32;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+      }
+      if (i < m) cw.pre[i] = carry + inc - l32;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (carry > CERT_EMAX) m = -1;
+    if (lane == 0) {
+      cw.m = m;
+      cw.E = carry;
+      if (m > 0) cw.pre[m] = carry;
+    }
+  }
+  for (int i = threadIdx.x; i < CERT_M * CERT_W; i += blockDim.x) cw.rows[i] = 0u;
+  __syncthreads();
+  const int m = cw.m, E = cw.E;
+  if (m <= 0) {
+    __syncthreads();
+    return m < 0 ? -1 : 0;
+  }
+  // flattened walk over the CTA: entry e of the concatenated member rows
+  for (int e0 = 0; e0 < E; e0 += (int)blockDim.x * CERT_U) {
+    int32_t w[CERT_U];
+    int own[CERT_U];
+#pragma unroll
+    for (int u = 0; u < CERT_U; ++u) {
+      const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+      w[u] = -1;
+      own[u] = 0;
+      if (e < E) {
+        int lo = 0, hi = m;  // owner: last i with pre[i] <= e
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (cw.pre[mid] <= e) lo = mid; else hi = mid;
+        }
+        own[u] = lo;
+        w[u] = col[cw.start[lo] + (e - cw.pre[lo])];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CERT_U; ++u) {
+      if (w[u] < 0 || w[u] == v) continue;
+      int lo = 0, hi = m;  // w among the members (ascending)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cw.mem[mid] < w[u]) lo = mid + 1; else hi = mid;
+      }
+      if (lo < m && cw.mem[lo] == w[u])
+        atomicOr(&cw.rows[own[u] * CERT_W + (lo >> 5)], 1u << (lo & 31));
+    }
+  }
+  __syncthreads();
+  int cert = 0;
+  if (threadIdx.x < 32) {
+    // v (index m) is adjacent to every member
+    const int tot = m + 1;
+    int dg[CERT_W];
+    unsigned alive = 0;
+#pragma unroll
+    for (int q = 0; q < CERT_W; ++q) {
+      const int i = lane + 32 * q;
+      dg[q] = 0x7fff;
+      if (i < m) {
+        int c = 1;
+#pragma unroll
+        for (int x = 0; x < CERT_W; ++x) c += __popc(cw.rows[i * CERT_W + x]);
+        dg[q] = c;
+        alive |= 1u << q;
+      } else if (i == m) {
+        dg[q] = m;
+        alive |= 1u << q;
+      }
+    }
+    // min-degree peel: the certificate is the largest minimum degree seen
+    for (int left = tot; left - 1 > cert; --left) {
+      int key = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < CERT_W; ++q)
+        if ((alive >> q) & 1u) key = min(key, (dg[q] << 8) | (lane + 32 * q));
+      key = __reduce_min_sync(0xffffffffu, key);
+      const int md = key >> 8, j = key & 255;
+      cert = max(cert, md);
+      if ((j & 31) == lane) alive &= ~(1u << (j >> 5));
+#pragma unroll
+      for (int q = 0; q < CERT_W; ++q) {
+        const int i = lane + 32 * q;
+        bool adj;
+        if (j == m) adj = i < m;
+        else if (i == m) adj = true;
+        else adj = (cw.rows[j * CERT_W + q] >> lane) & 1u;
+        if (((alive >> q) & 1u) && adj) dg[q]--;
+      }
+    }
+  }
+  __syncthreads();
+  return cert;
+}
 
 // The tail kernel's own counters (zeroed by the host).
 struct PeelTailState {
@@ -580,7 +743,8 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
              int32_t* __restrict__ deg, int32_t* alive_a, int32_t* alive_b,
              uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
              int32_t* __restrict__ order, APeelShared* sh, int64_t* __restrict__ out_degeneracy,
-             unsigned poll_mask, unsigned sleep_ns, unsigned long long* trace, int64_t tail_max) {
+             unsigned poll_mask, unsigned sleep_ns, unsigned long long* trace, int64_t tail_max,
+             int k_floor) {
   const unsigned int G = gridDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * APEEL_THREADS + threadIdx.x;
@@ -603,7 +767,9 @@ k_peel_async(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, in
   int32_t* alive = alive_a;
   int32_t* alive2 = alive_b;
   int64_t na = n;
-  int32_t k = 0x7fffffff - *(volatile int*)&sh->mindeg0, deg_max = 0;
+  // the first level: the minimum degree, or the density floor when higher
+  // (k_floor = ceil(m / n) <= degeneracy, see peel_async)
+  int32_t k = max(0x7fffffff - *(volatile int*)&sh->mindeg0, k_floor), deg_max = 0;
   for (;;) {
     // few vertices left: the remaining levels go to one thread-block cluster
     // (k_peel_tail) -- here every level pays two grid-wide barriers
@@ -826,7 +992,8 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
               uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
               unsigned* __restrict__ rbits, int32_t* __restrict__ order, APeelShared* sh,
               int64_t* __restrict__ out_degeneracy, unsigned poll_mask, unsigned sleep_ns,
-              int64_t tail_max) {
+              int64_t tail_max, int k_floor, int64_t cert_n) {
+  __shared__ CertCta s_cert;
   const unsigned int G = gridDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * APEEL_THREADS + threadIdx.x;
@@ -849,12 +1016,15 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
   int32_t* alive = alive_a;
   int32_t* alive2 = alive_b;
   int64_t na = n;
-  int32_t k = 0x7fffffff - *(volatile int*)&sh->mindeg0, deg_max = 0;
+  // the first level: the minimum degree, or the density floor when higher
+  // (k_floor = ceil(m / n) <= degeneracy, see peel_async)
+  int32_t k = max(0x7fffffff - *(volatile int*)&sh->mindeg0, k_floor), deg_max = 0;
   // test-and-set claim of v: true for exactly one caller
   auto claim = [&](int32_t v) {
     const unsigned bit = 1u << (v & 31);
     return !(atomicOr(&rbits[v >> 5], bit) & bit);
   };
+  bool cert_done = cert_n <= 0;
   for (;;) {
     const unsigned vc0 = *(volatile unsigned*)&sh->vclaim;
     if (tail_max > 0 && n - (int64_t)vc0 <= tail_max) {  // see k_peel_async
@@ -866,6 +1036,44 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
         sh->tail = 1;
       }
       break;
+    }
+    // ---- residual jump (once, when at most cert_n vertices and n / 16 are
+    // left).  The remaining levels of a small residual cost a barrier and a
+    // scan each for little work (planted1m: 31 levels of planted cliques).
+    // A certificate c <= d (the best degeneracy of a sampled vertex's live
+    // closed neighbourhood) lets the threshold jump to c at once.  A vertex
+    // still leaves with at most min(its degree, c) <= d later neighbours, so
+    // the widest root class is unchanged; a vertex of core number k' < c may
+    // get up to c instead of k'.  The jump is taken only when no residual
+    // vertex has degree above 4c: a residual dominated by hubs (an R-MAT
+    // core) keeps the level-by-level peel.
+    if (!cert_done && na <= cert_n && na * 16 <= n) {
+      cert_done = true;
+      if (gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh->cert_t[0]));
+      const int64_t stride = (na + G - 1) / G;  // one sample per CTA
+      int mx = 0;
+      for (int64_t i = gtid; i < na; i += gstride) {
+        const int32_t v = __ldcg(&alive[i]);
+        if (cert_live(rbits, v)) mx = max(mx, (int)__ldcg(&deg[v]));
+      }
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if (lane == 0 && mx) atomicMax(&sh->cert_maxdeg, mx);
+      const int64_t i = (int64_t)blockIdx.x * stride;
+      if (i < na) {
+        const int32_t v = __ldcg(&alive[i]);
+        if (cert_live(rbits, v)) {  // uniform over the CTA
+          const int c = peel_certificate(ro, col, rbits, v, s_cert);
+          if (threadIdx.x == 0 && c > 0) atomicMax(&sh->cert, c);
+        }
+      }
+      agrid_barrier(sh, G, nothing);
+      const int c = *(volatile int*)&sh->cert;
+      if (gtid == 0) {
+        sh->cert_k0 = k;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh->cert_t[1]));
+      }
+      if (*(volatile int*)&sh->cert_maxdeg <= 4 * c) k = max(k, c);
+      if (gtid == 0) sh->cert_k1 = k;
     }
     // ---- scan (consumers may already be decrementing)
     constexpr int SCAN_U = 8;
@@ -992,7 +1200,10 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
     if ((int64_t)vc >= n) break;
     k = claimed ? k + 1 : max(k + 1, mn);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *out_degeneracy = deg_max;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *out_degeneracy = deg_max;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh->cert_t[2]));
+  }
 }
 
 // ---- the asynchronous peel on ONE thread-block cluster, for the last levels
@@ -1829,6 +2040,22 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
     MCE_CHECK(cudaMemsetAsync(ts, 0, sizeof(PeelTailState), s));
     MCE_CHECK(cudaMemsetAsync(queue, 0xff, sizeof(int32_t) * PEEL_TAIL_MAX, s));
   }
+  // Density floor.  A graph with degeneracy d has m <= d * n edges (each
+  // vertex has at most d later neighbours), so d >= ceil(m / n): every level
+  // below that threshold can be merged into ONE level at it.  Any vertex then
+  // leaves with at most ceil(m / n) <= d later neighbours -- still a valid
+  // degeneracy order with the same degeneracy (the d-core's vertices keep
+  // degree >= d until a level at d takes them) -- and the first levels'
+  // barriers and alive-list scans are skipped (planted1m: levels 3 .. 11
+  // collapse into level 12).  A vertex of core c < ceil(m / n) may then get
+  // up to ceil(m / n) later neighbours instead of c, so the floor is capped
+  // (MCE_PEEL_DENS_CAP, default 32: such roots stay in the |P| <= 32 class).
+  const int64_t dens_cap = (int64_t)apeel_env("MCE_PEEL_DENS_CAP", 32);
+  const int64_t m_edges = g->nnz / 2;
+  const int k_floor =
+      n > 0 ? (int)std::min<int64_t>((m_edges + n - 1) / n, dens_cap) : 0;
+  // residual jump of k_peel_async1 (MCE_PEEL_CERT = residual size, 0 disables)
+  const int64_t cert_n = (int64_t)apeel_env("MCE_PEEL_CERT", 65536);
   // one barrier per level (k_peel_async1) unless the per-level trace is on
   // or MCE_PEEL_MERGED=0 (diagnostics)
   const bool merged = !trace && apeel_env("MCE_PEEL_MERGED", 1) != 0;
@@ -1838,16 +2065,26 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
     k_peel_async1<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                       removed, rbits, order, sh, d_degeneracy,
                                                       apeel_env("MCE_APEEL_POLL", 3),
-                                                      apeel_env("MCE_APEEL_SLEEP", 32), tail_max);
+                                                      apeel_env("MCE_APEEL_SLEEP", 32), tail_max,
+                                                      k_floor, cert_n);
   } else {
     k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                      removed, order, sh, d_degeneracy,
                                                      apeel_env("MCE_APEEL_POLL", 3),
                                                      apeel_env("MCE_APEEL_SLEEP", 32), trace,
-                                                     tail_max);
+                                                     tail_max, k_floor);
   }
   mce_count_launch();
   MCE_CHECK(cudaGetLastError());
+  if (merged && getenv("MCE_PEEL_CERT_TRACE")) {  // diagnostics
+    APeelShared h{};
+    MCE_CHECK(cudaMemcpyAsync(&h, sh, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MCE_CHECK(cudaStreamSynchronize(s));
+    fprintf(stderr, "[peel cert] cert=%d residual_maxdeg=%d k %d -> %d; cert phase %.1f us, "
+                    "after it %.1f us\n", h.cert, h.cert_maxdeg, h.cert_k0, h.cert_k1,
+            h.cert_t[0] ? (h.cert_t[1] - h.cert_t[0]) / 1e3 : -1.0,
+            h.cert_t[0] ? (h.cert_t[2] - h.cert_t[1]) / 1e3 : -1.0);
+  }
   if (tail_max > 0) {
     k_peel_tail<<<PEEL_TAIL_CLUSTER, PEEL_TAIL_THREADS, 0, s>>>(
         g->ro, g->col, n, deg, alive, alive2, removed, order, sh, ts, lidx, gid, queue,

@@ -55,6 +55,12 @@ struct mce_graph {
   // table's event (stream-ordered) before reading it
   uint64_t* vhash_tab[2] = {nullptr, nullptr};
   cudaEvent_t vhash_ev[2] = {nullptr, nullptr};
+  // the N+ lists alone, packed (built once, like vhash, by the first
+  // enumeration): up_col[up_off[v], up_off[v+1]) = N+(v).  The induced-row
+  // builds read only N+ lists; packed they are half the CSR and stay in L2
+  int64_t* up_off = nullptr;  // n + 1
+  int32_t* up_col = nullptr;  // nnz / 2
+  cudaEvent_t up_ev = nullptr;
 };
 
 int mce_graph_build_split(mce_graph* g, cudaStream_t s);

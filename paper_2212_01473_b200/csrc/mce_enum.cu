@@ -106,6 +106,8 @@ struct EnumArgs {
   const int64_t* ro;
   const int32_t* col;
   const int64_t* split;
+  const int64_t* up_off;  // packed N+ lists (mce_graph::up_off / up_col)
+  const int32_t* up_col;
   const uint64_t* vhash;  // mix64(label(v))
   const int64_t* roots;   // l1: vertex, l2: (u << 32) | v
   int64_t num_roots;
@@ -381,7 +383,7 @@ struct Worker {
   // ---------------------------------------------------------------- flat walk
   template <typename RangeF, typename VisitF>
   __device__ __forceinline__ void flat_walk(int cnt, RangeF range, VisitF visit) const {
-    warp_flat_walk(a.col, lane, cnt, range, visit);
+    warp_flat_walk(a.up_col, lane, cnt, range, visit);  // N+ lists only
   }
 
   // ---------------------------------------------------------------- build
@@ -481,8 +483,8 @@ struct Worker {
         np + (xwalk ? nx : 0),
         [&](int i, int64_t& lo, int& len) {
           const int32_t m = i < np ? plist[i] : root_x[i - np];
-          lo = a.split[m];
-          len = (int)(a.ro[m + 1] - lo);
+          lo = a.up_off[m];
+          len = (int)(a.up_off[m + 1] - lo);
         },
         [&](int i, int32_t w) {
           if (i < np) {
@@ -2204,6 +2206,27 @@ __global__ void k_later_count(const int64_t* __restrict__ ro, const int64_t* __r
     out[v] = ro[v + 1] - split[v];
 }
 
+// up_col[up_off[v] ..] = N+(v): one thread per row (rows are short; a warp
+// per row would walk 1M rows in dependent offset-load chains)
+__global__ void k_pack_upper(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
+                             const int32_t* __restrict__ col, const int64_t* __restrict__ up_off,
+                             int64_t n, int32_t* __restrict__ up_col) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = split[v], len = ro[v + 1] - s0, o = up_off[v];
+    int64_t k = 0;
+    for (; k + 4 <= len; k += 4) {
+      const int32_t a0 = __ldcs(&col[s0 + k]), a1 = __ldcs(&col[s0 + k + 1]);
+      const int32_t a2 = __ldcs(&col[s0 + k + 2]), a3 = __ldcs(&col[s0 + k + 3]);
+      up_col[o + k] = a0;
+      up_col[o + k + 1] = a1;
+      up_col[o + k + 2] = a2;
+      up_col[o + k + 3] = a3;
+    }
+    for (; k < len; ++k) up_col[o + k] = __ldcs(&col[s0 + k]);
+  }
+}
+
 __global__ void k_vhash(const int64_t* __restrict__ labels, int64_t n, uint64_t* __restrict__ vh) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x)
@@ -2564,6 +2587,34 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
     }
   }
   const uint64_t* vhash = gm->vhash_tab[want_labels];
+  {  // the packed N+ lists (same once-per-graph rule)
+    static std::mutex up_mu;
+    std::lock_guard<std::mutex> lk(up_mu);
+    if (!gm->up_off) {
+      int64_t *off = nullptr, *later = nullptr;
+      int32_t* ucol = nullptr;
+      if (dalloc(&off, n + 1, s) || dalloc(&ucol, std::max<int64_t>(g->nnz / 2, 1), s) ||
+          get(&later, n))
+        return -1;
+      k_later_count<<<grid_for(n), 256, 0, s>>>(g->ro, g->split, n, later);
+      mce_count_launch();
+      MCE_CHECK(cudaMemsetAsync(off, 0, sizeof(int64_t), s));
+      size_t tb = 0;
+      MCE_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tb, later, off + 1, n, s));
+      void* tmp = nullptr;
+      if (scr.raw(&tmp, tb)) return -1;
+      MCE_CHECK(cub::DeviceScan::InclusiveSum(tmp, tb, later, off + 1, n, s));
+      k_pack_upper<<<grid_for(n), 256, 0, s>>>(g->ro, g->split, g->col, off, n, ucol);
+      mce_count_launch();
+      MCE_CHECK(cudaGetLastError());
+      MCE_CHECK(cudaEventCreateWithFlags(&gm->up_ev, cudaEventDisableTiming));
+      MCE_CHECK(cudaEventRecord(gm->up_ev, s));
+      gm->up_col = ucol;
+      gm->up_off = off;
+    } else {
+      MCE_CHECK(cudaStreamWaitEvent(s, gm->up_ev, 0));
+    }
+  }
   int64_t metric_slots = 0;
   {
     int dev = 0, sms = 0;
@@ -2744,6 +2795,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
       args.ro = g->ro;
       args.col = g->col;
       args.split = g->split;
+      args.up_off = g->up_off;
+      args.up_col = g->up_col;
       args.vhash = vhash;
       args.roots = sorted_roots + cp.begin;
       args.num_roots = cp.count;
@@ -2790,6 +2843,8 @@ int mce_enumerate(const mce_graph* g, const mce_run_config* cfg, int64_t* collec
         ta.ro = g->ro;
         ta.col = g->col;
         ta.split = g->split;
+        ta.up_off = g->up_off;
+        ta.up_col = g->up_col;
         ta.vhash = vhash;
         ta.roots = sorted_roots + cp.begin;
         ta.num_roots = cp.count;

@@ -2399,6 +2399,9 @@ void mce_graph_free(mce_graph* g) {
     if (g->vhash_tab[t]) cudaFreeAsync(g->vhash_tab[t], 0);
     if (g->vhash_ev[t]) cudaEventDestroy(g->vhash_ev[t]);
   }
+  if (g->up_off) cudaFreeAsync(g->up_off, 0);
+  if (g->up_col) cudaFreeAsync(g->up_col, 0);
+  if (g->up_ev) cudaEventDestroy(g->up_ev);
   if (g->stats_slot) {
     StatsSlot* sl = static_cast<StatsSlot*>(g->stats_slot);
     cudaEventSynchronize(sl->ev);  // its copy must land before the slot is reused

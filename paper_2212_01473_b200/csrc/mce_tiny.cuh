@@ -68,6 +68,8 @@ struct TinyArgs {
   const int64_t* ro;
   const int32_t* col;
   const int64_t* split;
+  const int64_t* up_off;             // packed N+ lists (mce_graph::up_off / up_col)
+  const int32_t* up_col;
   const uint64_t* vhash;
   const int64_t* roots;
   int64_t num_roots;
@@ -373,11 +375,11 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
           m = spl[r * TINY_STRIDE + k];
           info = r | (k << 6) | (rbase << 12);
         } else {
-          m = __ldg(&col[xr + (k - npr)]);
+          m = __ldcs(&col[xr + (k - npr)]);  // the root's own N-: read once
           info = r | 32 | ((k - npr) << 6) | ((rbase + npr) << 12);
         }
-        lo = __ldg(&a.split[m]);
-        len = (int)(__ldg(&a.ro[m + 1]) - lo);
+        lo = __ldg(&a.up_off[m]);
+        len = (int)(__ldg(&a.up_off[m + 1]) - lo);
       }
       // flatten the 32 members' N+ lists over the lanes (see warp_flat_walk)
       int inc2 = len;
@@ -404,7 +406,7 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
           const int64_t lo_o = __shfl_sync(FULLMASK, lo, o);
           const int ex_o = __shfl_sync(FULLMASK, exc2, o);
           inf[u] = __shfl_sync(FULLMASK, info, o);
-          val[u] = kk < tot2 ? __ldg(&col[lo_o + (kk - ex_o)]) : 0x7fffffff;
+          val[u] = kk < tot2 ? __ldg(&a.up_col[lo_o + (kk - ex_o)]) : 0x7fffffff;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {

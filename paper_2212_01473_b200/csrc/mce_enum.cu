@@ -2206,24 +2206,41 @@ __global__ void k_later_count(const int64_t* __restrict__ ro, const int64_t* __r
     out[v] = ro[v + 1] - split[v];
 }
 
-// up_col[up_off[v] ..] = N+(v): one thread per row (rows are short; a warp
-// per row would walk 1M rows in dependent offset-load chains)
+// up_col[up_off[v] ..] = N+(v).  A warp packs 32 consecutive rows: their
+// destinations are one contiguous range, written coalesced, each entry's
+// source row found by a 5-step shuffle search over the rows' offsets
 __global__ void k_pack_upper(const int64_t* __restrict__ ro, const int64_t* __restrict__ split,
                              const int32_t* __restrict__ col, const int64_t* __restrict__ up_off,
                              int64_t n, int32_t* __restrict__ up_col) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s0 = split[v], len = ro[v + 1] - s0, o = up_off[v];
-    int64_t k = 0;
-    for (; k + 4 <= len; k += 4) {
-      const int32_t a0 = __ldcs(&col[s0 + k]), a1 = __ldcs(&col[s0 + k + 1]);
-      const int32_t a2 = __ldcs(&col[s0 + k + 2]), a3 = __ldcs(&col[s0 + k + 3]);
-      up_col[o + k] = a0;
-      up_col[o + k + 1] = a1;
-      up_col[o + k + 2] = a2;
-      up_col[o + k + 3] = a3;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; v0 < n;
+       v0 += nw * 32) {
+    const int64_t v = v0 + lane;
+    const int64_t src = v < n ? split[v] : 0;
+    const int64_t o = v < n ? up_off[v] : INT64_MAX;
+    const int64_t obeg = __shfl_sync(0xffffffffu, o, 0);
+    const int64_t oend = up_off[v0 + 32 < n ? v0 + 32 : n];
+    constexpr int U = 4;  // loads in flight per lane
+    for (int64_t base = obeg; base < oend; base += 32 * U) {
+      int32_t val[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = base + 32 * u + lane;
+        int r = 0;  // last row whose range starts at or before j
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int64_t t = __shfl_sync(0xffffffffu, o, r + step);
+          if (t <= j) r += step;
+        }
+        const int64_t sr = __shfl_sync(0xffffffffu, src, r);
+        const int64_t orr = __shfl_sync(0xffffffffu, o, r);
+        val[u] = j < oend ? __ldcs(&col[sr + (j - orr)]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + 32 * u + lane < oend) up_col[base + 32 * u + lane] = val[u];
     }
-    for (; k < len; ++k) up_col[o + k] = __ldcs(&col[s0 + k]);
   }
 }
 

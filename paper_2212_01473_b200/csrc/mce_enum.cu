@@ -53,6 +53,15 @@ namespace {
 #define MCE_CMP_NARROW_MAX_W 1
 #endif
 constexpr int HIST_SMEM = 128;
+
+// 128-bit blocked bloom filter over a root's P (k_tiny's induced-row walk
+// tests every N+ entry against P; most miss): bit 31 of the hash picks the
+// 64-bit word, bits 19-24 and 25-30 the two bits set / tested in it.  (The
+// same filter in the warp kernels' walk measured slower: 1.70 -> 1.74 ms.)
+__device__ __forceinline__ uint32_t bloom_hash(int32_t w) { return (uint32_t)w * 0x9E3779B1u; }
+__device__ __forceinline__ unsigned long long bloom_bits(uint32_t h) {
+  return (1ull << ((h >> 19) & 63)) | (1ull << ((h >> 25) & 63));
+}
 #ifndef MCE_TEAM_REMOTE_MIN_P
 #define MCE_TEAM_REMOTE_MIN_P 48
 #endif

@@ -61,7 +61,7 @@ constexpr int TINY_SPILL = 33 - TINY_DEPTH;  // global frames (a pushed level ho
 #define MCE_TINY_M_MAX 16
 #endif
 constexpr int TINY_M_MAX = MCE_TINY_M_MAX;
-constexpr int TINY_WARP_WORDS = TINY_SLICE + TINY_POOL + 64;  // + 32 bloom words (64-bit)
+constexpr int TINY_WARP_WORDS = TINY_SLICE + TINY_POOL + 128;  // + 32 x 2 bloom words (64-bit)
 constexpr int TINY_SMEM_WORDS = HIST_SMEM + TINY_WARP_WORDS * TINY_WARPS;
 
 struct TinyArgs {
@@ -260,7 +260,7 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
   const int lane = threadIdx.x & 31;
   int32_t* spl = reinterpret_cast<int32_t*>(tsm + HIST_SMEM) + warp * TINY_WARP_WORDS;
   unsigned long long* sbloom = reinterpret_cast<unsigned long long*>(spl + TINY_SLICE);
-  uint32_t* spool = reinterpret_cast<uint32_t*>(spl + TINY_SLICE + 64);
+  uint32_t* spool = reinterpret_cast<uint32_t*>(spl + TINY_SLICE + 128);
   for (int i = threadIdx.x; i < HIST_SMEM; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
   const int gw = (int)((blockIdx.x * TINY_THREADS + threadIdx.x) >> 5);
@@ -346,10 +346,16 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
       if (q < total && k < npr) spl[r * TINY_STRIDE + k] = __ldg(&col[sr + k]);
     }
     __syncwarp();
-    {  // 64-bit bloom filter of the root's members: most N+ entries miss P
-      unsigned long long bl = 0;
-      for (int k = 0; k < np; ++k) bl |= 1ull << (mypl[k] & 63);
-      sbloom[lane] = bl;
+    {  // 128-bit blocked bloom filter of the root's members (two bits in one
+       // of two words): most N+ entries miss P, and a miss skips the search
+      unsigned long long b0 = 0, b1 = 0;
+      for (int k = 0; k < np; ++k) {
+        const uint32_t h = bloom_hash(mypl[k]);
+        const unsigned long long bits = bloom_bits(h);
+        if (h >> 31) b1 |= bits; else b0 |= bits;
+      }
+      sbloom[2 * lane] = b0;
+      sbloom[2 * lane + 1] = b1;
     }
     __syncwarp();
     for (int q0 = 0; q0 < total; q0 += 32) {
@@ -412,7 +418,9 @@ __global__ void __maxnreg__(MCE_TINY_MAXREG) k_tiny(TinyArgs a) {
         for (int u = 0; u < U; ++u) {
           if (b2 + u * 32 + lane < tot2) {
             const int rr = inf[u] & 31;
-            if ((sbloom[rr] >> (val[u] & 63)) & 1ull) {
+            const uint32_t h = bloom_hash(val[u]);
+            const unsigned long long bits = bloom_bits(h);
+            if ((sbloom[2 * rr + (h >> 31)] & bits) == bits) {
               const int j = tiny_find(spl + rr * TINY_STRIDE, val[u]);
               if (j >= 0) {
                 const int ii = (inf[u] >> 6) & 63;

@@ -1,6 +1,6 @@
 #!/bin/bash
-# Round-2 evidence on the GPU box: bench lines, launch list, ncu captures of
-# the enumeration kernels and the peel.  usage: tools/r2_profile.sh <tag>
+# Round-3 evidence on the GPU box: bench lines, launch list, ncu captures of
+# the enumeration kernels and the peel.  usage: tools/r3_profile.sh <tag>
 tag=${1:-x}
 mkdir -p gpurun_out
 python -m paper_2212_01473_b200.build > /dev/null 2>&1
@@ -27,7 +27,7 @@ for f in ncu_enum_planted1m_$tag ncu_enum_ba200k_$tag ncu_peel_planted1m_$tag; d
 done
 cp profiles/traffic.json gpurun_out/traffic_$tag.json
 for w in planted1m ba200k; do
-  python tools/traffic_from_ncu.py $w $R/ncu_enum_${w}_$tag.ncu-rep r2/ncu_enum_${w}_$tag.txt > /dev/null 2>&1
+  python tools/traffic_from_ncu.py $w $R/ncu_enum_${w}_$tag.ncu-rep r3/ncu_enum_${w}_$tag.txt > /dev/null 2>&1
 done
 cp profiles/traffic.json gpurun_out/traffic_$tag.json
 ls -la gpurun_out | grep $tag

@@ -483,6 +483,8 @@ struct APeelShared {
   int cert_maxdeg;                        // max degree of the residual it was taken on
   int cert_k0, cert_k1;                   // diagnostics: threshold before / after the jump
   unsigned long long cert_t[3];           // diagnostics: globaltimer at start / cert / end
+  unsigned long long lvl[64][3];          // diagnostics: per level (k, end time, positions)
+  unsigned int nlvl;
 };
 
 // ---- degeneracy certificate (k_peel_async1's residual jump).  The
@@ -992,7 +994,7 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
               uint64_t* __restrict__ tasks, uint8_t* __restrict__ removed,
               unsigned* __restrict__ rbits, int32_t* __restrict__ order, APeelShared* sh,
               int64_t* __restrict__ out_degeneracy, unsigned poll_mask, unsigned sleep_ns,
-              int64_t tail_max, int k_floor, int64_t cert_n) {
+              int64_t tail_max, int k_floor, int64_t cert_n, int slack) {
   __shared__ CertCta s_cert;
   const unsigned int G = gridDim.x;
   const int lane = threadIdx.x & 31;
@@ -1009,6 +1011,7 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
     removed[v] = 0;
   }
   for (int64_t w = gtid; w < (n + 31) / 32; w += gstride) rbits[w] = 0;
+  if (gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh->cert_t[2]));
   dmin = __reduce_min_sync(0xffffffffu, dmin);
   if (lane == 0 && dmin != 0x7fffffff) atomicMax(&sh->mindeg0, 0x7fffffff - dmin);
   if (gtid == 0) sh->mindeg = 0x7fffffff;  // the rest of *sh is zeroed by the host
@@ -1025,6 +1028,41 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
     return !(atomicOr(&rbits[v >> 5], bit) & bit);
   };
   bool cert_done = cert_n <= 0;
+  // one sampled live vertex per CTA: its closed neighbourhood's degeneracy
+  // max-reduced into sh->cert (a lower bound on d); with `maxdeg`, also the
+  // residual's maximum degree into sh->cert_maxdeg.  Callers barrier after.
+  auto certify = [&](const int32_t* al, int64_t cnt, bool maxdeg) {
+    const int64_t stride = (cnt + G - 1) / G;
+    if (maxdeg) {
+      int mx = 0;
+      for (int64_t i = gtid; i < cnt; i += gstride) {
+        const int32_t v = __ldcg(&al[i]);
+        if (cert_live(rbits, v)) mx = max(mx, (int)__ldcg(&deg[v]));
+      }
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if (lane == 0 && mx) atomicMax(&sh->cert_maxdeg, mx);
+    }
+    const int64_t i = (int64_t)blockIdx.x * stride;
+    if (i < cnt) {
+      const int32_t v = __ldcg(&al[i]);
+      if (cert_live(rbits, v)) {  // uniform over the CTA
+        const int c = peel_certificate(ro, col, rbits, v, s_cert);
+        if (threadIdx.x == 0 && c > 0) atomicMax(&sh->cert, c);
+      }
+    }
+  };
+  // Level slack: a level may claim up to `slack` above its level number k
+  // while that stays <= a certified lower bound `dlb` of d (the density
+  // floor, then a certificate sampled over the residual after the first
+  // level -- a graph peeled in one level pays nothing).  A vertex then
+  // leaves with at most core + slack later neighbours (never above d), and
+  // consecutive levels whose cascades are long merge into one (planted1m:
+  // 13, the bulk level 14 and 15 become one level).  Taking the certificate
+  // before the first level too (merging 12 as well) measured 35 us faster on
+  // planted1m but costs a graph peeled in one level (ba200k) 25 us.
+  int dlb = k_floor;
+  bool slack_cert = slack > 0;
+  int levels = 0;
   for (;;) {
     const unsigned vc0 = *(volatile unsigned*)&sh->vclaim;
     if (tail_max > 0 && n - (int64_t)vc0 <= tail_max) {  // see k_peel_async
@@ -1050,24 +1088,10 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
     if (!cert_done && na <= cert_n && na * 16 <= n) {
       cert_done = true;
       if (gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh->cert_t[0]));
-      const int64_t stride = (na + G - 1) / G;  // one sample per CTA
-      int mx = 0;
-      for (int64_t i = gtid; i < na; i += gstride) {
-        const int32_t v = __ldcg(&alive[i]);
-        if (cert_live(rbits, v)) mx = max(mx, (int)__ldcg(&deg[v]));
-      }
-      mx = __reduce_max_sync(0xffffffffu, mx);
-      if (lane == 0 && mx) atomicMax(&sh->cert_maxdeg, mx);
-      const int64_t i = (int64_t)blockIdx.x * stride;
-      if (i < na) {
-        const int32_t v = __ldcg(&alive[i]);
-        if (cert_live(rbits, v)) {  // uniform over the CTA
-          const int c = peel_certificate(ro, col, rbits, v, s_cert);
-          if (threadIdx.x == 0 && c > 0) atomicMax(&sh->cert, c);
-        }
-      }
+      certify(alive, na, true);
       agrid_barrier(sh, G, nothing);
       const int c = *(volatile int*)&sh->cert;
+      dlb = max(dlb, c);
       if (gtid == 0) {
         sh->cert_k0 = k;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(sh->cert_t[1]));
@@ -1075,6 +1099,14 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
       if (*(volatile int*)&sh->cert_maxdeg <= 4 * c) k = max(k, c);
       if (gtid == 0) sh->cert_k1 = k;
     }
+    if (slack_cert && levels > 0 && k + slack > dlb) {
+      slack_cert = false;
+      certify(alive, na, false);
+      agrid_barrier(sh, G, nothing);
+      dlb = max(dlb, *(volatile int*)&sh->cert);
+    }
+    // this level's threshold: k plus the slack, within the certified bound
+    const int32_t t = max(k, min(k + slack, dlb));
     // ---- scan (consumers may already be decrementing)
     constexpr int SCAN_U = 8;
     for (int64_t base = (gtid - lane) * SCAN_U; base < na; base += gstride * SCAN_U) {
@@ -1096,8 +1128,8 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
 #pragma unroll
       for (int u = 0; u < SCAN_U; ++u) {
         const bool live = v[u] >= 0 && !((rb[u] >> (v[u] & 31)) & 1u);
-        const bool take = live && d[u] <= k && claim(v[u]);
-        const bool keep = live && d[u] > k;
+        const bool take = live && d[u] <= t && claim(v[u]);
+        const bool keep = live && d[u] > t;
         km[u] = __ballot_sync(0xffffffffu, keep);
         nkeep += __popc(km[u]);
         if (keep) md = min(md, (int)d[u]);
@@ -1128,7 +1160,7 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
     __threadfence();  // this warp's claims are counted before its scan is
     if (lane == 0) atomicAdd(&sh->scans_done, 1u);
     // ---- consume chunks until every scan is done and nothing is in flight
-    const int32_t kp1 = k + 1;
+    const int32_t kp1 = t + 1;
     bool over = false;
     while (!over) {
       unsigned long long h = 0;
@@ -1190,15 +1222,24 @@ k_peel_async1(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, i
       alive2 = t;
     }
     const bool claimed = vc > vc0;
-    if (claimed) deg_max = max(deg_max, k);
-    agrid_barrier(sh, G, [sh] {
+    if (claimed) deg_max = max(deg_max, t);
+    agrid_barrier(sh, G, [sh, t, vc] {
       sh->head = sh->tclaim;
       sh->scans_done = 0;
       sh->acount = 0;
       sh->mindeg = 0x7fffffff;
+      if (sh->nlvl < 64) {  // diagnostics (MCE_PEEL_CERT_TRACE prints them)
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        sh->lvl[sh->nlvl][0] = (unsigned long long)t;
+        sh->lvl[sh->nlvl][1] = now;
+        sh->lvl[sh->nlvl][2] = vc;
+        sh->nlvl++;
+      }
     });
     if ((int64_t)vc >= n) break;
-    k = claimed ? k + 1 : max(k + 1, mn);
+    k = claimed ? t + 1 : max(t + 1, mn);
+    ++levels;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *out_degeneracy = deg_max;
@@ -2056,6 +2097,8 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
       n > 0 ? (int)std::min<int64_t>((m_edges + n - 1) / n, dens_cap) : 0;
   // residual jump of k_peel_async1 (MCE_PEEL_CERT = residual size, 0 disables)
   const int64_t cert_n = (int64_t)apeel_env("MCE_PEEL_CERT", 65536);
+  // level slack of k_peel_async1 (MCE_PEEL_SLACK, 0 disables)
+  const int slack = (int)apeel_env("MCE_PEEL_SLACK", 2);
   // one barrier per level (k_peel_async1) unless the per-level trace is on
   // or MCE_PEEL_MERGED=0 (diagnostics)
   const bool merged = !trace && apeel_env("MCE_PEEL_MERGED", 1) != 0;
@@ -2066,7 +2109,7 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
                                                       removed, rbits, order, sh, d_degeneracy,
                                                       apeel_env("MCE_APEEL_POLL", 3),
                                                       apeel_env("MCE_APEEL_SLEEP", 32), tail_max,
-                                                      k_floor, cert_n);
+                                                      k_floor, cert_n, slack);
   } else {
     k_peel_async<<<(int)grid, APEEL_THREADS, 0, s>>>(g->ro, g->col, n, deg, alive, alive2, tasks,
                                                      removed, order, sh, d_degeneracy,
@@ -2084,6 +2127,9 @@ int peel_async(const mce_graph* g, int64_t* d_pos, int64_t* d_degeneracy, cudaSt
                     "after it %.1f us\n", h.cert, h.cert_maxdeg, h.cert_k0, h.cert_k1,
             h.cert_t[0] ? (h.cert_t[1] - h.cert_t[0]) / 1e3 : -1.0,
             h.cert_t[0] ? (h.cert_t[2] - h.cert_t[1]) / 1e3 : -1.0);
+    for (unsigned i = 0; i < h.nlvl && i < 64; ++i)
+      fprintf(stderr, "[peel level] k=%llu end %.1f us positions %llu\n", h.lvl[i][0],
+              i ? (h.lvl[i][1] - h.lvl[0][1]) / 1e3 : 0.0, h.lvl[i][2]);
   }
   if (tail_max > 0) {
     k_peel_tail<<<PEEL_TAIL_CLUSTER, PEEL_TAIL_THREADS, 0, s>>>(

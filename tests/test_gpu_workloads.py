@@ -367,13 +367,28 @@ def test_bench_two_ranks_reproduce_one_gpu(shard, tmp_path):
     import subprocess
     import sys
 
+    import socket
+
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, MCE_BENCH_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + (shard == "steal")),
-           os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "ba200k", "--steps", "3",
-           "--warmup", "3", "--shard", shard, "--no-cpu-baseline", "--no-clocks"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
+
+    def launch():
+        with socket.socket() as sk:  # a free rendezvous port
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(port),
+               os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "ba200k", "--steps", "3",
+               "--warmup", "3", "--shard", shard, "--no-cpu-baseline", "--no-clocks"]
+        return subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root, env=env)
+
+    # two processes time-slicing one GPU next to this one's context: one
+    # full-suite run saw a launch never return (not reproducible alone, 17 s);
+    # a stalled launch is retried once on a fresh port
+    try:
+        out = launch()
+    except subprocess.TimeoutExpired:
+        out = launch()
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["result"]["sharding"] == shard

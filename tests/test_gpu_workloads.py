@@ -245,6 +245,47 @@ def test_async_peel_is_a_degeneracy_order(name, tail, monkeypatch):
         (rp.clique_count, rp.clique_hash, rp.size_histogram)
 
 
+@pytest.mark.parametrize("env", [{"MCE_PEEL_SLACK": "0"}, {"MCE_PEEL_CERT": "0"},
+                                 {"MCE_PEEL_DENS_CAP": "0"},
+                                 {"MCE_PEEL_SLACK": "0", "MCE_PEEL_CERT": "0", "MCE_PEEL_DENS_CAP": "0"},
+                                 {"MCE_PEEL_SLACK": "6"}])
+def test_async_peel_certified_jumps(env, monkeypatch):
+    """The async peel's certified shortcuts one at a time (density floor,
+    level slack, residual certificate jump): a sparse background of 200k
+    vertices plus disjoint planted cliques of 10-80 members, so the residual
+    is small, clique-made and its certificate the largest clique's size - 1.
+    Every variant is a valid degeneracy order with the reference's
+    degeneracy and the same clique set."""
+    from paper_2212_01473_b200 import degeneracy_order
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(7)
+    n0 = 200_000
+    bg = rng.integers(0, n0, size=(3 * n0, 2), dtype=np.int64)
+    parts, base = [bg], n0
+    for size in range(10, 81, 5):
+        for _ in range(4):
+            u, w = np.triu_indices(size, k=1)
+            parts.append(np.column_stack((u + base, w + base)))
+            base += size
+    edges = np.concatenate(parts)
+    g = from_edges(edges, base)
+    ro, ci = g.row_offsets, g.col_indices
+    _, d = oracle.degeneracy_order(ro, ci)
+    assert d == 79
+    for _ in range(2):
+        got = degeneracy_order(g, method="async")
+        assert got.degeneracy == d
+        assert np.array_equal(np.sort(got.position), np.arange(base))
+        assert _later_counts(ro, ci, got.position).max() == d
+    g_a, _, st_a = preprocess(g, method="async")
+    g_p, _, st_p = preprocess(g, method="parallel")
+    ra, rp = run(g_a, st_a, RunConfig()), run(g_p, st_p, RunConfig())
+    assert (ra.clique_count, ra.clique_hash, ra.size_histogram) == \
+        (rp.clique_count, rp.clique_hash, rp.size_histogram)
+
+
 def test_async_peel_on_reference_graphs():
     """Every golden graph of the reference's tests: valid degeneracy order,
     exact degeneracy, and the reference's clique count / hash."""

@@ -1820,16 +1820,42 @@ k_canon_long_rows(const int64_t* __restrict__ rs, int32_t* __restrict__ buf,
 }
 
 // row v's ucnt[v] deduplicated entries from buf[rs[v] ..) to col[ro[v] ..)
+// Deduplicated rows into the final CSR.  A warp moves 32 consecutive rows:
+// their destinations are one contiguous range, written coalesced, each
+// entry's source row found by a 5-step shuffle search over the rows' offsets
+// (a warp per row waited on two offset loads for every ~20-entry row).
 __global__ void k_compact_rows(const int64_t* __restrict__ rs, const int64_t* __restrict__ ro,
                                const int32_t* __restrict__ buf, int64_t n,
                                int32_t* __restrict__ col) {
   const int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    const int64_t src = rs[v], dst = ro[v];
-    const int d = (int)(ro[v + 1] - dst);
-    for (int i = lane; i < d; i += 32) col[dst + i] = buf[src + i];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; v0 < n;
+       v0 += nw * 32) {
+    const int64_t v = v0 + lane;
+    const int64_t src = v < n ? rs[v] : 0;
+    const int64_t o = v < n ? ro[v] : INT64_MAX;
+    const int64_t obeg = __shfl_sync(0xffffffffu, o, 0);
+    const int64_t oend = ro[v0 + 32 < n ? v0 + 32 : n];
+    constexpr int U = 4;  // loads in flight per lane
+    for (int64_t base = obeg; base < oend; base += 32 * U) {
+      int32_t val[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = base + 32 * u + lane;
+        int r = 0;  // last row whose range starts at or before j
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int64_t t = __shfl_sync(0xffffffffu, o, r + step);
+          if (t <= j) r += step;
+        }
+        const int64_t sr = __shfl_sync(0xffffffffu, src, r);
+        const int64_t orr = __shfl_sync(0xffffffffu, o, r);
+        val[u] = j < oend ? buf[sr + (j - orr)] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + 32 * u + lane < oend) col[base + 32 * u + lane] = val[u];
+    }
   }
 }
 
@@ -1924,7 +1950,7 @@ int canon_rows(mce_graph* g, const T* d_edges, int64_t num_edges, cudaStream_t s
   g->nnz = nnz;
   if (dev_alloc(&g->col, std::max<int64_t>(nnz, 1), s)) return -1;
   if (nnz > 0) {
-    k_compact_rows<<<grid_for(n * 32), 256, 0, s>>>(rs, g->ro, buf, n, g->col);
+    k_compact_rows<<<grid_for(n), 256, 0, s>>>(rs, g->ro, buf, n, g->col);
     mce_count_launch();
   }
   MCE_CHECK(cudaGetLastError());

@@ -499,7 +499,7 @@ struct APeelShared {
 constexpr int CERT_M = 128;               // members (v last)
 constexpr int CERT_W = CERT_M / 32;       // bitset words per row
 constexpr int64_t CERT_EMAX = 8192;       // adjacency entries walked per sample
-constexpr int CERT_U = 4;                 // entry loads in flight per thread
+constexpr int CERT_U = 8;                 // entry loads in flight per thread
 struct CertCta {
   int32_t mem[CERT_M];      // live neighbours of v, ascending
   int32_t pre[CERT_M + 1];  // exclusive prefix of the members' row lengths
@@ -536,14 +536,19 @@ __device__ int peel_certificate(const int64_t* __restrict__ ro, const int32_t* _
     __syncwarp();
     // row lengths and starts, exclusive prefix over the members
     int carry = 0;
-    for (int q = 0; m > 0 && q < CERT_W; ++q) {
+    int64_t qa[CERT_W], ql[CERT_W];  // every slot's offsets loaded before any scan
+#pragma unroll
+    for (int q = 0; q < CERT_W; ++q) {
       const int i = lane + 32 * q;
-      int64_t a = 0, len = 0;
-      if (i < m) {
-        a = ro[cw.mem[i]];
-        len = ro[cw.mem[i] + 1] - a;
-        cw.start[i] = a;
-      }
+      qa[q] = i < m ? ro[cw.mem[i]] : 0;
+      ql[q] = i < m ? ro[cw.mem[i] + 1] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < CERT_W; ++q) {
+      if (m <= 0) break;
+      const int i = lane + 32 * q;
+      const int64_t a = qa[q], len = i < m ? ql[q] - a : 0;
+      if (i < m) cw.start[i] = a;
       const int l32 = (int)(len < CERT_EMAX ? len : CERT_EMAX);
       int inc = l32;
 #pragma unroll
